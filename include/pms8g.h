@@ -1,0 +1,141 @@
+/* include/pms8g.h — C ABI of the B200-native PMS8 per-S1-l-mer search.
+ *
+ * Drop-in boundary for the reference's solver entry points (the reference has
+ * no FFI layer of its own); every function below names the
+ * reference interface it replaces (paths relative to /root/reference/proj).
+ *
+ *   pms8g_solve          <- pms8::run_parallel   include/pms8/parallel.hpp:37-38
+ *                           pms8::solve          include/pms8/solver.hpp:180
+ *   pms8g_result_free    <- (ownership of MotifSet, solver.hpp:19)
+ *   pms8g_ctx_*          <- SolverContext ctor   include/pms8/solver.hpp:65-85 (device-resident,
+ *                           re-runnable context: inputs stay in HBM between runs)
+ *   pms8g_generate       <- generate_planted_instance include/pms8/instance.hpp:38
+ *   pms8g_estimate_threshold <- estimate_threshold include/pms8/solver.hpp:61
+ *   pms8g_merge_keys     <- canonical_motif_set  include/pms8/solver.hpp:22 (device sort+unique
+ *                           of packed motif keys; used after the multi-GPU allgather)
+ *
+ * Plain pointers and sizes only. All calls are blocking unless stated, own
+ * their CUDA streams, and never fall back to the CPU: without a usable sm_100
+ * device they fail with PMS8G_ERR_CUDA. Errors mirror the reference's three
+ * exception classes (invalid_argument / runtime_error / logic_error); the
+ * message is written to err (NUL-terminated, truncated to errlen).
+ */
+#ifndef PMS8G_H
+#define PMS8G_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PMS8G_OK = 0,
+    PMS8G_ERR_INVALID = 1, /* std::invalid_argument (Problem::validate src/problem.cpp:7-28, threshold src/solver.cpp:137) */
+    PMS8G_ERR_RUNTIME = 2, /* std::runtime_error (motif cap src/solver.cpp:382-384, allocation) */
+    PMS8G_ERR_LOGIC = 3,   /* std::logic_error (reverify failure src/solver.cpp:376) */
+    PMS8G_ERR_CUDA = 4     /* device missing / launch failure (no CPU fallback exists) */
+};
+
+/* Mirrors SolverConfig (include/pms8/solver.hpp:24-31) plus the device and
+ * sharding knobs that replace ParallelOptions (include/pms8/parallel.hpp:22-28). */
+typedef struct pms8g_options {
+    int threshold;         /* 0: GPU-tuned default; else 1..n (SolverConfig::threshold_override) */
+    int sort_rows;         /* 1: branch on the smallest row (reference default) */
+    int prune_level;       /* 0 none, 1 pairs, 2 full (PruneLevel, neighborhood.hpp:16-20) */
+    int reverify;          /* re-check every motif against all windows (reverify_against_originals) */
+    int64_t max_motifs;    /* -1: unlimited; raw emissions above it -> PMS8G_ERR_RUNTIME */
+    int device;            /* CUDA device ordinal; -1: current device */
+    int shard_rank;        /* S1 offsets j with j % shard_count == shard_rank are searched */
+    int shard_count;       /* 0 or 1: no sharding */
+    const int32_t* anchors; /* optional explicit S1 offsets (subset runs), NULL: all */
+    int nanchors;
+    int warps_per_block;   /* 0: default */
+    int blocks_per_sm;     /* 0: default */
+} pms8g_options;
+
+/* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */
+typedef struct pms8g_report {
+    int n, m, l, d, sigma;
+    int threshold;          /* switch depth actually used */
+    int gpus;               /* devices used by this call (1) */
+    int64_t subproblems;    /* S1 l-mers searched by this call */
+    int64_t motif_count;    /* unique motifs returned */
+    double wall_seconds;    /* host wall clock of the call */
+    double device_seconds;  /* CUDA-event time of the device pipeline */
+    double sample_seconds;  /* row build + filter share (device clock estimate) */
+    double pattern_seconds; /* enumerate + verify share (device clock estimate) */
+    int64_t stacks_explored; /* l-mers pushed (counting the anchor) */
+    int64_t neighborhoods;   /* tuples enumerated */
+    int64_t neighbors_visited; /* candidates generated */
+    int64_t motifs_emitted;  /* raw verified candidates (pre-dedup) */
+    int64_t filter_slots;    /* l-mer slots tested by push filters (incl. row build) */
+    int64_t verify_compares; /* candidate x l-mer Hamming compares in verification */
+    int64_t enum_nodes;      /* enumeration tree nodes expanded */
+    uint64_t device_bytes;   /* device memory held by the context */
+} pms8g_report;
+
+/* Motifs as uppercase strings of length l, concatenated without separators,
+ * sorted and deduplicated (canonical_motif_set order). */
+typedef struct pms8g_result {
+    int64_t count;
+    int l;
+    char* motifs;           /* count*l chars (+NUL), owned; free with pms8g_result_free */
+    pms8g_report report;
+} pms8g_result;
+
+void pms8g_default_options(pms8g_options* opt);
+
+/* Whole-instance (or shard / subset) search from HOST codes.
+ * codes: n*m bytes, row-major, values in [0, sigma) (sigma <= 4; symbols come
+ * from `alphabet`, e.g. "ACGT", used only to decode motifs). */
+int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt,
+                pms8g_result* out, char* err, size_t errlen);
+void pms8g_result_free(pms8g_result* r);
+
+/* Device-resident context: allocate once, load codes (host or device pointer),
+ * run many times. Keys: 128-bit MSB-first 2-bit packing of each motif (symbol
+ * 0 in the highest used bits), so integer order == lexicographic order; stored
+ * as two uint64 {lo, hi} per key. */
+typedef struct pms8g_ctx pms8g_ctx;
+int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt, pms8g_ctx** out,
+                     char* err, size_t errlen);
+int pms8g_ctx_load_codes(pms8g_ctx* ctx, const uint8_t* codes, int codes_on_device, char* err, size_t errlen);
+/* Runs encode -> row build -> persistent search -> device sort/unique on the
+ * context's stream and waits for it. */
+int pms8g_ctx_run(pms8g_ctx* ctx, char* err, size_t errlen);
+/* Device pointer to the unique sorted keys of the last run and their count. */
+int pms8g_ctx_keys(pms8g_ctx* ctx, const uint64_t** dev_keys, int64_t* count);
+/* Copies the motifs of the last run to the host (like pms8g_solve's result). */
+int pms8g_ctx_result(pms8g_ctx* ctx, pms8g_result* out, char* err, size_t errlen);
+void* pms8g_ctx_stream(pms8g_ctx* ctx); /* cudaStream_t */
+/* Dedicated event pair around the main search kernel of the last launch. */
+int pms8g_ctx_kernel_ms(pms8g_ctx* ctx, float* search_ms, float* rowbuild_ms);
+void pms8g_ctx_destroy(pms8g_ctx* ctx);
+
+/* Device sort+unique of `count` keys (2 x uint64 each) at dev_in into dev_out
+ * (capacity >= count); returns the unique count. Both device pointers. */
+int pms8g_merge_keys(const uint64_t* dev_in, int64_t count, uint64_t* dev_out, int64_t* out_count, void* stream,
+                     char* err, size_t errlen);
+/* Host decode of keys into strings (count*l chars, caller-allocated). */
+void pms8g_decode_keys(const uint64_t* host_keys, int64_t count, int l, const char* alphabet, char* out);
+
+/* Planted instance generator (src/instance.cpp:22-73), byte-identical stream. */
+int pms8g_generate(int n, int m, int l, int d, int sigma, uint64_t seed, int exactly_d, uint8_t* codes_out,
+                   uint8_t* motif_out, int32_t* positions_out);
+/* Threshold model (src/solver.cpp:75-117) and the GPU-tuned default. */
+int pms8g_estimate_threshold(int n, int m, int l, int d, int sigma);
+int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma);
+
+/* Integer-pipe peak microbenchmark: LOP3/IADD3-class ops per second over all
+ * SMs of `device` (measured, used as the roofline denominator), and the SM
+ * clock (MHz) the device reported while it ran. */
+int pms8g_int_peak(int device, double* ops_per_second, double* popc_per_second, char* err, size_t errlen);
+
+const char* pms8g_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,741 @@
+// pms8g_capi.cu — the C ABI (include/pms8g.h): validation, device context,
+// pipeline orchestration on one CUDA stream, CUB sort/unique, host decode.
+//
+// Mirrors the reference's run_parallel (src/parallel.cpp:35-118): build the
+// shared context once (here: encode + per-anchor row build on the device),
+// search every S1 l-mer (here: one persistent kernel over a global work queue
+// of (S1 l-mer, depth-1 branch) tasks), then canonicalise the motif set
+// (sort + unique, src/solver.cpp:16-21). There is no CPU search path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/pms8g.h"
+#include "pms8g_device.cuh"
+#include "pms8g_launch.h"
+
+using namespace pms8g;
+
+namespace {
+
+struct Err {
+    int code = PMS8G_OK;
+    std::string msg;
+};
+
+int fail(char* err, size_t errlen, int code, const char* fmt, ...) {
+    if (err && errlen) {
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(err, errlen, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CU(call)                                                                                               \
+    do {                                                                                                       \
+        cudaError_t e__ = (call);                                                                              \
+        if (e__ != cudaSuccess)                                                                                \
+            return fail(err, errlen, PMS8G_ERR_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorName(e__), \
+                        __FILE__, __LINE__, cudaGetErrorString(e__));                                          \
+    } while (0)
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+unsigned __int128 nsize(int l, int d, int sigma) {
+    unsigned __int128 total = 0, binom = 1, power = 1;
+    for (int i = 0; i <= d; ++i) {
+        total += binom * power;
+        binom = binom * static_cast<unsigned>(l - i) / static_cast<unsigned>(i + 1);
+        power *= static_cast<unsigned>(sigma - 1);
+    }
+    return total;
+}
+
+}  // namespace
+
+struct pms8g_ctx {
+    int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
+    std::string alphabet;
+    pms8g_options opt{};
+    std::vector<int32_t> anchors;
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    uint8_t* d_codes = nullptr;
+    void* d_table = nullptr;
+    int32_t* d_anchors = nullptr;
+    uint32_t* d_l1 = nullptr;
+    LevelMeta* d_meta = nullptr;
+    long long* d_task_base = nullptr;
+    unsigned long long* d_task_counter = nullptr;
+    uint32_t* d_scratch = nullptr;
+    size_t scratch_words = 0;
+    int level_cap = 0, node_cap = 0;
+    unsigned long long* d_keys = nullptr;
+    unsigned long long* d_keys_sorted = nullptr;
+    unsigned long long* d_keys_unique = nullptr;
+    long long key_cap = 0;
+    unsigned long long* d_key_count = nullptr;
+    long long* d_unique_count = nullptr;
+    void* d_cub = nullptr;
+    size_t cub_bytes = 0;
+    unsigned long long* d_counters = nullptr;
+    int* d_err = nullptr;
+    int* d_fail = nullptr;
+    // pinned host mirrors
+    unsigned long long* h_counters = nullptr;  // C_NCTR + 1 (key count)
+    int* h_err = nullptr;
+    int blocks = 0, warps = 0;
+    size_t smem = 0;
+    size_t device_bytes = 0;
+    long long unique_count = 0;
+    pms8g_report report{};
+};
+
+namespace {
+
+int alloc(pms8g_ctx* c, void** p, size_t bytes, char* err, size_t errlen) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e != cudaSuccess)
+        return fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate %zu bytes of device memory: %s", bytes,
+                    cudaGetErrorString(e));
+    c->device_bytes += bytes;
+    return PMS8G_OK;
+}
+
+int ensure_key_capacity(pms8g_ctx* c, long long need, char* err, size_t errlen) {
+    if (need <= c->key_cap) return PMS8G_OK;
+    long long cap = std::max<long long>(need, 2 * c->key_cap);
+    cudaFree(c->d_keys);
+    cudaFree(c->d_keys_sorted);
+    cudaFree(c->d_keys_unique);
+    cudaFree(c->d_cub);
+    c->d_keys = c->d_keys_sorted = c->d_keys_unique = nullptr;
+    c->d_cub = nullptr;
+    int rc;
+    if ((rc = alloc(c, reinterpret_cast<void**>(&c->d_keys), 16 * cap, err, errlen))) return rc;
+    if ((rc = alloc(c, reinterpret_cast<void**>(&c->d_keys_sorted), 16 * cap, err, errlen))) return rc;
+    if ((rc = alloc(c, reinterpret_cast<void**>(&c->d_keys_unique), 16 * cap, err, errlen))) return rc;
+    size_t b1 = 0, b2 = 0;
+    using K128 = unsigned __int128;
+    cub::DeviceRadixSort::SortKeys(nullptr, b1, reinterpret_cast<K128*>(c->d_keys),
+                                   reinterpret_cast<K128*>(c->d_keys_sorted), static_cast<int>(cap), 0,
+                                   std::max(1, 2 * c->l));
+    cub::DeviceSelect::Unique(nullptr, b2, reinterpret_cast<K128*>(c->d_keys_sorted),
+                              reinterpret_cast<K128*>(c->d_keys_unique), c->d_unique_count, static_cast<int>(cap));
+    c->cub_bytes = std::max(b1, b2);
+    if ((rc = alloc(c, &c->d_cub, c->cub_bytes, err, errlen))) return rc;
+    c->key_cap = cap;
+    return PMS8G_OK;
+}
+
+int validate_problem(int n, int m, int l, int d, const char* alphabet, char* err, size_t errlen, int* sigma) {
+    // Problem::validate, src/problem.cpp:7-28
+    if (n < 1) return fail(err, errlen, PMS8G_ERR_INVALID, "no input sequences");
+    if (l < 1) return fail(err, errlen, PMS8G_ERR_INVALID, "motif length must be >= 1");
+    if (l > m) return fail(err, errlen, PMS8G_ERR_INVALID, "motif length %d exceeds sequence length %d", l, m);
+    if (d < 0 || d > l) return fail(err, errlen, PMS8G_ERR_INVALID, "mismatch budget must be in [0, l], got %d", d);
+    const int s = alphabet ? static_cast<int>(std::strlen(alphabet)) : 4;
+    if (s < 2) return fail(err, errlen, PMS8G_ERR_INVALID, "alphabet needs at least 2 symbols");
+    // GPU path limits: 2 bit planes, 32 rows per warp table,
+    // 24-bit l-mer ids, 16-bit row offsets
+    if (s > 4)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 4 symbols, got %d", s);
+    if (l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
+    if (n > MAXN) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n <= %d sequences, got %d", MAXN, n);
+    const long long K = static_cast<long long>(n) * (m - l + 1);
+    if (K > 65535) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n*(m-l+1) <= 65535, got %lld", K);
+    *sigma = s;
+    return PMS8G_OK;
+}
+
+int resolve_threshold(int n, int m, int l, int d, int sigma, int requested, char* err, size_t errlen, int* t) {
+    if (requested != 0) {
+        if (requested < 1 || requested > n)
+            return fail(err, errlen, PMS8G_ERR_INVALID, "threshold must be in [1, n], got %d", requested);
+        *t = requested;
+    } else {
+        *t = pms8g_gpu_threshold(n, m, l, d, sigma);
+    }
+    // the output is independent of t (every pruning rule is sound); the
+    // device tables hold at most MAXT stack members
+    if (*t > MAXT) *t = MAXT;
+    if (*t > n) *t = n;
+    if (*t < 1) *t = 1;
+    return PMS8G_OK;
+}
+
+int run_pipeline(pms8g_ctx* c, char* err, size_t errlen);
+
+}  // namespace
+
+extern "C" {
+
+void pms8g_default_options(pms8g_options* o) {
+    std::memset(o, 0, sizeof *o);
+    o->sort_rows = 1;
+    o->prune_level = 2;
+    o->device = -1;
+    o->shard_count = 1;
+    o->max_motifs = -1;
+}
+
+const char* pms8g_version(void) { return "pms8g 0.1 (sm_100a)"; }
+
+int pms8g_estimate_threshold(int n, int m, int l, int d, int sigma) {
+    // threshold_curve + estimate_threshold, src/solver.cpp:75-117
+    if (n < 2) return n;
+    if (m == l) return n;
+    if (m <= l) return 2;
+    auto lg = [](unsigned __int128 v) { return static_cast<double>(std::log(static_cast<long double>(v))); };
+    const double log_nd = lg(nsize(l, d, sigma));
+    const double log_n2d = lg(nsize(l, std::min(2 * d, l), sigma));
+    const double log_p = log_n2d - l * std::log(static_cast<double>(sigma));
+    const double log_q = log_nd - log_n2d;
+    const double log_w = std::log(static_cast<double>(m - l + 1));
+    std::vector<double> terms;
+    for (int k = 1; k <= n; ++k) terms.push_back(k * log_w + 0.5 * k * (k - 1) * log_p);
+    int best_t = 2;
+    double best = INFINITY;
+    for (int t = 2; t <= n; ++t) {
+        const double mx = *std::max_element(terms.begin(), terms.begin() + t);
+        double sum = 0;
+        for (int k = 0; k < t; ++k) sum += std::exp(terms[k] - mx);
+        const double ls = std::log(static_cast<double>(n)) + std::log(static_cast<double>(l)) + mx + std::log(sum);
+        const double lp = terms[t - 1] + log_nd + (t - 1) * log_q + std::log(static_cast<double>(l));
+        const double v = std::max(ls, lp);
+        if (v < best - 1e-12) {
+            best = v;
+            best_t = t;
+        }
+    }
+    return best_t;
+}
+
+int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
+    if (const char* env = std::getenv("PMS8G_THRESHOLD")) {
+        const int v = std::atoi(env);
+        if (v >= 1) return std::min(v, n);
+    }
+    return pms8g_estimate_threshold(n, m, l, d, sigma);
+}
+
+int pms8g_generate(int n, int m, int l, int d, int sigma, uint64_t seed, int exactly_d, uint8_t* codes_out,
+                   uint8_t* motif_out, int32_t* positions_out) {
+    // generate_planted_instance, src/instance.cpp:12-73: std::mt19937_64 +
+    // rejection-sampled bounded draws, same draw order
+    if (l < 1 || l > m || d < 0 || d > l || n < 1 || sigma < 2) return PMS8G_ERR_INVALID;
+    std::mt19937_64 rng(seed);
+    auto draw = [&](uint64_t bound) {
+        const uint64_t threshold = (~bound + 1) % bound;
+        for (;;) {
+            const uint64_t x = rng();
+            if (x >= threshold) return x % bound;
+        }
+    };
+    for (int p = 0; p < l; ++p) motif_out[p] = static_cast<uint8_t>(draw(sigma));
+    std::vector<int> columns(l);
+    std::vector<uint8_t> occ(l);
+    for (int i = 0; i < n; ++i) {
+        uint8_t* seq = codes_out + static_cast<size_t>(i) * m;
+        for (int j = 0; j < m; ++j) seq[j] = static_cast<uint8_t>(draw(sigma));
+        const int pos = static_cast<int>(draw(static_cast<uint64_t>(m - l + 1)));
+        std::memcpy(occ.data(), motif_out, l);
+        for (int j = 0; j < l; ++j) columns[j] = j;
+        for (int j = 0; j < d; ++j) {
+            const int pick = j + static_cast<int>(draw(static_cast<uint64_t>(l - j)));
+            std::swap(columns[j], columns[pick]);
+            const int col = columns[j];
+            if (!exactly_d) {
+                occ[col] = static_cast<uint8_t>(draw(sigma));
+            } else {
+                uint64_t cc = draw(static_cast<uint64_t>(sigma - 1));
+                if (cc >= occ[col]) ++cc;
+                occ[col] = static_cast<uint8_t>(cc);
+            }
+        }
+        std::memcpy(seq + pos, occ.data(), l);
+        positions_out[i] = pos;
+    }
+    return PMS8G_OK;
+}
+
+int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt_in, pms8g_ctx** out,
+                     char* err, size_t errlen) {
+    *out = nullptr;
+    pms8g_options opt;
+    if (opt_in) opt = *opt_in;
+    else pms8g_default_options(&opt);
+    int sigma = 0;
+    int rc = validate_problem(n, m, l, d, alphabet, err, errlen, &sigma);
+    if (rc) return rc;
+    int t = 0;
+    if ((rc = resolve_threshold(n, m, l, d, sigma, opt.threshold, err, errlen, &t))) return rc;
+    if (opt.shard_count < 1) opt.shard_count = 1;
+    if (opt.shard_rank < 0 || opt.shard_rank >= opt.shard_count)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "shard rank %d outside [0, %d)", opt.shard_rank, opt.shard_count);
+
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "no CUDA device available (%s); the GPU path has no CPU fallback",
+                    cudaGetErrorString(ce));
+    int dev = opt.device;
+    if (dev < 0) CU(cudaGetDevice(&dev));
+    if (dev >= ndev) return fail(err, errlen, PMS8G_ERR_INVALID, "device %d not present (%d devices)", dev, ndev);
+    CU(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100-class; kernels are sm_100a only",
+                    dev, prop.name, prop.major, prop.minor);
+
+    auto* c = new pms8g_ctx();
+    c->n = n;
+    c->m = m;
+    c->l = l;
+    c->d = d;
+    c->sigma = sigma;
+    c->alphabet = alphabet ? alphabet : "ACGT";
+    c->W = l <= 32 ? 1 : 2;
+    c->w = m - l + 1;
+    c->K = n * c->w;
+    c->t = t;
+    c->opt = opt;
+    c->device = dev;
+    c->sms = prop.multiProcessorCount;
+    // S1 offsets of this call (split_subproblems, src/parallel.cpp:14-20), sharded
+    if (opt.anchors && opt.nanchors > 0) {
+        for (int i = 0; i < opt.nanchors; ++i) {
+            const int a = opt.anchors[i];
+            if (a < 0 || a >= c->w) {
+                delete c;
+                return fail(err, errlen, PMS8G_ERR_INVALID, "anchor offset %d outside [0, %d)", a, c->w);
+            }
+            if (a % opt.shard_count == opt.shard_rank) c->anchors.push_back(a);
+        }
+    } else {
+        for (int a = 0; a < c->w; ++a)
+            if (a % opt.shard_count == opt.shard_rank) c->anchors.push_back(a);
+    }
+    c->opt.anchors = nullptr;
+    c->opt.nanchors = 0;
+
+    auto cleanup_fail = [&](int code) {
+        pms8g_ctx_destroy(c);
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot create stream"));
+    for (auto& e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess)
+            return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot create event"));
+
+    // launch shape: one persistent block per SM, as many warps as the
+    // shared-memory l-mer table leaves room for
+    const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    int warps = opt.warps_per_block > 0 ? opt.warps_per_block : 16;
+    while (warps > 1 && search_smem(c->W, c->K, warps) > smem_cap) --warps;
+    if (search_smem(c->W, c->K, warps) > smem_cap)
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
+                                 "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K, smem_cap));
+    c->warps = warps;
+    c->smem = search_smem(c->W, c->K, warps);
+    c->blocks = c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
+    if (set_search_smem(c->W, c->smem) != cudaSuccess)
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
+
+    const int na = static_cast<int>(c->anchors.size());
+    c->level_cap = c->K;
+    c->node_cap = 32 * (l + 2);
+    const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
+    const size_t node_words = static_cast<size_t>(c->node_cap) * node_bytes(c->W) / 4;
+    c->scratch_words = (lvl_words + node_words + 31) / 32 * 32;
+    const size_t nwarps_total = static_cast<size_t>(c->blocks) * warps;
+    int rc2;
+#define AL(ptr, bytes)                                                                          \
+    if ((rc2 = alloc(c, reinterpret_cast<void**>(&(ptr)), (bytes), err, errlen)) != PMS8G_OK) \
+        return cleanup_fail(rc2);
+    AL(c->d_codes, static_cast<size_t>(n) * m);
+    AL(c->d_table, static_cast<size_t>(c->K) * lmer_bytes(c->W));
+    AL(c->d_anchors, sizeof(int32_t) * std::max(1, na));
+    AL(c->d_l1, sizeof(uint32_t) * static_cast<size_t>(std::max(1, na)) * c->K);
+    AL(c->d_meta, sizeof(LevelMeta) * std::max(1, na));
+    AL(c->d_task_base, sizeof(long long) * (na + 1));
+    AL(c->d_task_counter, sizeof(unsigned long long));
+    AL(c->d_scratch, sizeof(uint32_t) * c->scratch_words * nwarps_total);
+    AL(c->d_key_count, sizeof(unsigned long long));
+    AL(c->d_unique_count, sizeof(long long));
+    AL(c->d_counters, sizeof(unsigned long long) * C_NCTR);
+    AL(c->d_err, sizeof(int));
+    AL(c->d_fail, sizeof(int));
+#undef AL
+    if (cudaMallocHost(reinterpret_cast<void**>(&c->h_counters), sizeof(unsigned long long) * (C_NCTR + 2)) !=
+            cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&c->h_err), sizeof(int) * 4) != cudaSuccess)
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate pinned host memory"));
+    if ((rc2 = ensure_key_capacity(c, 1 << 14, err, errlen)) != PMS8G_OK) return cleanup_fail(rc2);
+    if (na > 0 && cudaMemcpy(c->d_anchors, c->anchors.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice) !=
+                      cudaSuccess)
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "anchor upload failed"));
+    *out = c;
+    return PMS8G_OK;
+}
+
+void pms8g_ctx_destroy(pms8g_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->d_codes, c->d_table,      c->d_anchors,     c->d_l1,           c->d_meta,
+                    c->d_task_base, c->d_task_counter, c->d_scratch, c->d_keys,   c->d_keys_sorted,
+                    c->d_keys_unique, c->d_key_count, c->d_unique_count, c->d_cub, c->d_counters,
+                    c->d_err,     c->d_fail};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int pms8g_ctx_load_codes(pms8g_ctx* c, const uint8_t* codes, int on_device, char* err, size_t errlen) {
+    CU(cudaSetDevice(c->device));
+    const size_t bytes = static_cast<size_t>(c->n) * c->m;
+    if (!on_device) {
+        for (size_t i = 0; i < bytes; ++i)
+            if (codes[i] >= c->sigma)
+                return fail(err, errlen, PMS8G_ERR_INVALID, "sequence %zu, position %zu: code %d not in alphabet %s",
+                            i / c->m, i % c->m, codes[i], c->alphabet.c_str());
+    }
+    CU(cudaMemcpyAsync(c->d_codes, codes, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       c->stream));
+    return PMS8G_OK;
+}
+
+void* pms8g_ctx_stream(pms8g_ctx* c) { return c ? c->stream : nullptr; }
+
+int pms8g_ctx_run(pms8g_ctx* c, char* err, size_t errlen) { return run_pipeline(c, err, errlen); }
+
+int pms8g_ctx_keys(pms8g_ctx* c, const uint64_t** dev_keys, int64_t* count) {
+    *dev_keys = reinterpret_cast<const uint64_t*>(c->d_keys_unique);
+    *count = c->unique_count;
+    return PMS8G_OK;
+}
+
+int pms8g_ctx_kernel_ms(pms8g_ctx* c, float* search_ms, float* rowbuild_ms) {
+    float a = 0, b = 0;
+    if (cudaEventElapsedTime(&a, c->ev[2], c->ev[3]) != cudaSuccess) a = -1;
+    if (cudaEventElapsedTime(&b, c->ev[0], c->ev[1]) != cudaSuccess) b = -1;
+    if (search_ms) *search_ms = a;
+    if (rowbuild_ms) *rowbuild_ms = b;
+    return PMS8G_OK;
+}
+
+void pms8g_decode_keys(const uint64_t* keys, int64_t count, int l, const char* alphabet, char* out) {
+    const char* sym = alphabet ? alphabet : "ACGT";
+    for (int64_t i = 0; i < count; ++i) {
+        const uint64_t lo = keys[2 * i], hi = keys[2 * i + 1];
+        for (int p = 0; p < l; ++p) {
+            const int sh = 2 * (l - 1 - p);
+            const int code = static_cast<int>(((sh >= 64) ? (hi >> (sh - 64)) : (lo >> sh)) & 3u);
+            out[i * l + p] = sym[code];
+        }
+    }
+}
+
+int pms8g_ctx_result(pms8g_ctx* c, pms8g_result* out, char* err, size_t errlen) {
+    std::memset(out, 0, sizeof *out);
+    CU(cudaSetDevice(c->device));
+    const long long cnt = c->unique_count;
+    std::vector<uint64_t> keys(2 * static_cast<size_t>(std::max(0ll, cnt)));
+    if (cnt > 0) {
+        CU(cudaMemcpyAsync(keys.data(), c->d_keys_unique, 16 * cnt, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    out->l = c->l;
+    out->count = cnt;
+    out->motifs = static_cast<char*>(std::malloc(static_cast<size_t>(cnt) * c->l + 1));
+    if (!out->motifs) return fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate motif buffer");
+    pms8g_decode_keys(keys.data(), cnt, c->l, c->alphabet.c_str(), out->motifs);
+    out->motifs[static_cast<size_t>(cnt) * c->l] = 0;
+    out->report = c->report;
+    return PMS8G_OK;
+}
+
+void pms8g_result_free(pms8g_result* r) {
+    if (r && r->motifs) {
+        std::free(r->motifs);
+        r->motifs = nullptr;
+    }
+}
+
+int pms8g_merge_keys(const uint64_t* dev_in, int64_t count, uint64_t* dev_out, int64_t* out_count, void* stream,
+                     char* err, size_t errlen) {
+    using K128 = unsigned __int128;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    *out_count = 0;
+    if (count <= 0) return PMS8G_OK;
+    K128* tmp = nullptr;
+    long long* d_n = nullptr;
+    void* temp = nullptr;
+    size_t b1 = 0, b2 = 0;
+    CU(cudaMalloc(&tmp, sizeof(K128) * count));
+    CU(cudaMalloc(&d_n, sizeof(long long)));
+    cub::DeviceRadixSort::SortKeys(nullptr, b1, reinterpret_cast<const K128*>(dev_in), tmp, static_cast<int>(count),
+                                   0, 128, s);
+    cub::DeviceSelect::Unique(nullptr, b2, tmp, reinterpret_cast<K128*>(dev_out), d_n, static_cast<int>(count), s);
+    CU(cudaMalloc(&temp, std::max(b1, b2)));
+    size_t bytes = std::max(b1, b2);
+    CU(cub::DeviceRadixSort::SortKeys(temp, bytes, reinterpret_cast<const K128*>(dev_in), tmp,
+                                      static_cast<int>(count), 0, 128, s));
+    bytes = std::max(b1, b2);
+    CU(cub::DeviceSelect::Unique(temp, bytes, tmp, reinterpret_cast<K128*>(dev_out), d_n, static_cast<int>(count),
+                                 s));
+    long long n = 0;
+    CU(cudaMemcpyAsync(&n, d_n, sizeof n, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(d_n);
+    cudaFree(temp);
+    *out_count = n;
+    return PMS8G_OK;
+}
+
+namespace {
+std::mutex g_cache_mu;
+pms8g_ctx* g_cache = nullptr;
+
+bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alphabet, const pms8g_options& o) {
+    if (!c) return false;
+    const int dev = o.device;
+    int cur = -1;
+    if (dev < 0) cudaGetDevice(&cur);
+    return c->n == n && c->m == m && c->l == l && c->d == d && c->alphabet == (alphabet ? alphabet : "ACGT") &&
+           c->opt.threshold == o.threshold && c->opt.sort_rows == o.sort_rows && c->opt.prune_level == o.prune_level &&
+           c->opt.reverify == o.reverify && c->opt.max_motifs == o.max_motifs &&
+           c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
+           (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && c->opt.warps_per_block == o.warps_per_block &&
+           c->opt.blocks_per_sm == o.blocks_per_sm;
+}
+}  // namespace
+
+int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt_in,
+                pms8g_result* out, char* err, size_t errlen) {
+    const double t0 = now_s();
+    std::memset(out, 0, sizeof *out);
+    pms8g_options opt;
+    if (opt_in) opt = *opt_in;
+    else pms8g_default_options(&opt);
+    int sigma = 0;
+    int rc = validate_problem(n, m, l, d, alphabet, err, errlen, &sigma);
+    if (rc) return rc;
+    // a process-wide context cache keeps device buffers across calls of the
+    // same shape (like a cached library handle); subset runs are never cached
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    pms8g_ctx* c = nullptr;
+    bool cached = false;
+    if (same_shape(g_cache, n, m, l, d, alphabet, opt)) {
+        c = g_cache;
+        cached = true;
+    } else {
+        if ((rc = pms8g_ctx_create(n, m, l, d, alphabet, &opt, &c, err, errlen))) return rc;
+        if (!opt.anchors) {
+            pms8g_ctx_destroy(g_cache);
+            g_cache = c;
+            cached = true;
+        }
+    }
+    rc = pms8g_ctx_load_codes(c, codes, 0, err, errlen);
+    if (!rc) rc = pms8g_ctx_run(c, err, errlen);
+    if (!rc) rc = pms8g_ctx_result(c, out, err, errlen);
+    if (!cached) pms8g_ctx_destroy(c);
+    if (!rc) out->report.wall_seconds = now_s() - t0;
+    return rc;
+}
+
+int pms8g_int_peak(int device, double* ops_per_second, double* popc_per_second, char* err, size_t errlen) {
+    if (device >= 0) CU(cudaSetDevice(device));
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev));
+    uint32_t* sink = nullptr;
+    CU(cudaMalloc(&sink, 16));
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 2048;
+    double res[2] = {0, 0};
+    for (int which = 0; which < 2; ++which) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+            CU(cudaEventRecord(a));
+            CU(launch_intpeak(which, blocks, threads, iters, sink, nullptr));
+            CU(cudaEventRecord(b));
+            CU(cudaEventSynchronize(b));
+            float ms = 0;
+            CU(cudaEventElapsedTime(&ms, a, b));
+            if (rep > 0) best = std::min(best, ms);
+        }
+        const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+        res[which] = ops / (best * 1e-3);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (ops_per_second) *ops_per_second = res[0];
+    if (popc_per_second) *popc_per_second = res[1];
+    return PMS8G_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
+    const double t0 = now_s();
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const int na = static_cast<int>(c->anchors.size());
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        CU(cudaMemsetAsync(c->d_counters, 0, sizeof(unsigned long long) * C_NCTR, s));
+        CU(cudaMemsetAsync(c->d_key_count, 0, sizeof(unsigned long long), s));
+        CU(cudaMemsetAsync(c->d_task_counter, 0, sizeof(unsigned long long), s));
+        CU(cudaMemsetAsync(c->d_err, 0, sizeof(int), s));
+        CU(cudaMemsetAsync(c->d_fail, 0, sizeof(int), s));
+        CU(launch_encode(c->W, c->d_codes, c->n, c->m, c->l, c->w, c->d_table, c->d_err, s));
+        CU(cudaEventRecord(c->ev[0], s));
+        CU(launch_rowbuild(c->W, c->d_table, c->n, c->w, c->d, c->K, c->opt.sort_rows, c->d_anchors, na, c->d_l1,
+                           c->d_meta, c->d_counters, s));
+        CU(cudaEventRecord(c->ev[1], s));
+        CU(launch_taskscan(c->d_meta, na, c->t, c->d_task_base, s));
+        SearchParams P{};
+        P.n = c->n;
+        P.m = c->m;
+        P.l = c->l;
+        P.d = c->d;
+        P.w = c->w;
+        P.K = c->K;
+        P.t = c->t;
+        P.prune = c->opt.prune_level;
+        P.sort_rows = c->opt.sort_rows;
+        P.table = c->d_table;
+        P.l1_entries = c->d_l1;
+        P.l1_meta = c->d_meta;
+        P.anchor_off = c->d_anchors;
+        P.task_base = c->d_task_base;
+        P.nanchors = na;
+        P.task_counter = c->d_task_counter;
+        P.scratch = c->d_scratch;
+        P.scratch_words = c->scratch_words;
+        P.level_cap = c->level_cap;
+        P.node_cap = c->node_cap;
+        P.keys = c->d_keys;
+        P.key_count = c->d_key_count;
+        P.key_cap = c->key_cap;
+        P.counters = c->d_counters;
+        P.error_flag = c->d_err;
+        CU(cudaEventRecord(c->ev[2], s));
+        if (na > 0) CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
+        CU(cudaEventRecord(c->ev[3], s));
+        CU(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long) * C_NCTR, cudaMemcpyDeviceToHost,
+                           s));
+        CU(cudaMemcpyAsync(c->h_counters + C_NCTR, c->d_key_count, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        CU(cudaGetLastError());
+        if (c->h_err[0] & 1) return fail(err, errlen, PMS8G_ERR_INVALID, "symbol code outside the 2-bit alphabet");
+        if (c->h_err[0] & 2)
+            return fail(err, errlen, PMS8G_ERR_RUNTIME, "enumeration stack overflow (l=%d, capacity %d nodes)", c->l,
+                        c->node_cap);
+        const long long raw = static_cast<long long>(c->h_counters[C_NCTR]);
+        if (c->opt.max_motifs >= 0 && raw > c->opt.max_motifs)
+            return fail(err, errlen, PMS8G_ERR_RUNTIME, "motif cap of %lld exceeded",
+                        static_cast<long long>(c->opt.max_motifs));
+        if (raw > c->key_cap) {
+            int rc = ensure_key_capacity(c, raw + raw / 4 + 1024, err, errlen);
+            if (rc) return rc;
+            continue;  // rerun with room for every raw emission
+        }
+        // canonical_motif_set: device radix sort + unique
+        using K128 = unsigned __int128;
+        long long uniq = 0;
+        if (raw > 0) {
+            size_t bytes = c->cub_bytes;
+            CU(cub::DeviceRadixSort::SortKeys(c->d_cub, bytes, reinterpret_cast<K128*>(c->d_keys),
+                                              reinterpret_cast<K128*>(c->d_keys_sorted), static_cast<int>(raw), 0,
+                                              2 * c->l, s));
+            bytes = c->cub_bytes;
+            CU(cub::DeviceSelect::Unique(c->d_cub, bytes, reinterpret_cast<K128*>(c->d_keys_sorted),
+                                         reinterpret_cast<K128*>(c->d_keys_unique), c->d_unique_count,
+                                         static_cast<int>(raw), s));
+            CU(cudaMemcpyAsync(&c->h_counters[C_NCTR + 1], c->d_unique_count, sizeof(long long),
+                               cudaMemcpyDeviceToHost, s));
+            if (c->opt.reverify) {
+                CU(cudaStreamSynchronize(s));
+                uniq = static_cast<long long>(c->h_counters[C_NCTR + 1]);
+                CU(launch_reverify(c->W, c->d_table, c->n, c->w, c->l, c->d, c->d_keys_unique, uniq, c->d_fail, s));
+                CU(cudaMemcpyAsync(c->h_err + 1, c->d_fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+            }
+            CU(cudaStreamSynchronize(s));
+            uniq = static_cast<long long>(c->h_counters[C_NCTR + 1]);
+            if (c->opt.reverify && c->h_err[1])
+                return fail(err, errlen, PMS8G_ERR_LOGIC, "re-verification failed for a reported motif");
+        }
+        c->unique_count = uniq;
+        // report (RunReport fields, src/parallel.cpp:92-116)
+        pms8g_report& R = c->report;
+        std::memset(&R, 0, sizeof R);
+        R.n = c->n;
+        R.m = c->m;
+        R.l = c->l;
+        R.d = c->d;
+        R.sigma = c->sigma;
+        R.threshold = c->t;
+        R.gpus = 1;
+        R.subproblems = na;
+        R.motif_count = uniq;
+        const unsigned long long* h = c->h_counters;
+        R.stacks_explored = static_cast<int64_t>(h[C_PUSHES]);
+        R.neighborhoods = static_cast<int64_t>(h[C_TUPLES]);
+        R.neighbors_visited = static_cast<int64_t>(h[C_LEAVES]);
+        R.motifs_emitted = static_cast<int64_t>(h[C_EMITTED]);
+        R.filter_slots = static_cast<int64_t>(h[C_SLOTS]);
+        R.verify_compares = static_cast<int64_t>(h[C_VCMP]);
+        R.enum_nodes = static_cast<int64_t>(h[C_NODES]);
+        float ms_rb = 0, ms_search = 0;
+        cudaEventElapsedTime(&ms_rb, c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&ms_search, c->ev[2], c->ev[3]);
+        const double cf = static_cast<double>(h[C_CLK_FILTER]), cp = static_cast<double>(h[C_CLK_PATTERN]);
+        const double frac_pattern = (cf + cp) > 0 ? cp / (cf + cp) : 0.0;
+        R.device_seconds = (ms_rb + ms_search) * 1e-3;
+        R.pattern_seconds = ms_search * 1e-3 * frac_pattern;
+        R.sample_seconds = R.device_seconds - R.pattern_seconds;
+        R.device_bytes = c->device_bytes;
+        R.wall_seconds = now_s() - t0;
+        return PMS8G_OK;
+    }
+    return fail(err, errlen, PMS8G_ERR_RUNTIME, "motif buffer did not converge");
+}
+
+}  // namespace

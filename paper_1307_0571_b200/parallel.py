@@ -1,0 +1,135 @@
+"""Multi-GPU data parallelism over S1 l-mers: one process per GPU.
+
+Replaces the reference's OpenMP pull queue (src/parallel.cpp:35-118) and the
+paper's MPI scheduler/worker split. The m-l+1 S1 l-mers are
+independent subproblems (split_subproblems, src/parallel.cpp:14-20) whose motif
+sets union to the answer; rank r searches offsets j with j % world == r on its
+own GPU (cost per S1 l-mer varies by ~±15%, so an interleaved
+split balances without a data-path collective). The one exchange step is the
+union of the per-rank motif sets: an allgather of counts, then an allgather of
+padded 128-bit key buffers (NCCL over NVLink on GPUs, gloo in the CPU tests),
+followed by the device sort+unique of pms8g_merge_keys.
+"""
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+
+def distributed_world() -> int:
+    try:
+        import torch.distributed as dist
+    except Exception:
+        return 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size()
+    return 1
+
+
+def shard_offsets(num_offsets: int, rank: int, world: int):
+    """S1 offsets owned by `rank` (the same rule as pms8g_options.shard_*)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad shard {rank}/{world}")
+    return [j for j in range(num_offsets) if j % world == rank]
+
+
+def allgather_keys(local, group=None):
+    """Allgather of variable-length key tensors ([k, 2] int64 rows {lo, hi}).
+
+    Works for CUDA tensors (NCCL) and CPU tensors (gloo): counts first, then
+    buffers padded to the largest count. Returns the concatenation of every
+    rank's keys in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = local.device
+    cnt = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    cap = max(1, max(counts))
+    pad = torch.zeros((cap, 2), dtype=torch.int64, device=dev)
+    if local.shape[0]:
+        pad[: local.shape[0]] = local
+    bufs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+
+
+def merge_keys_device(keys):
+    """Device sort+unique (pms8g_merge_keys) of a CUDA [k, 2] int64 tensor."""
+    import torch
+    from . import _capi
+    k = int(keys.shape[0])
+    if k == 0:
+        return keys
+    keys = keys.contiguous()
+    out = torch.empty_like(keys)
+    n = ctypes.c_int64()
+    err = ctypes.create_string_buffer(512)
+    stream = torch.cuda.current_stream(keys.device).cuda_stream
+    rc = _capi.lib().pms8g_merge_keys(ctypes.c_void_p(keys.data_ptr()), k, ctypes.c_void_p(out.data_ptr()),
+                                      ctypes.byref(n), ctypes.c_void_p(stream), err, len(err))
+    if rc != 0:
+        from . import _raise
+        _raise(rc, err)
+    return out[: n.value]
+
+
+def decode_keys(keys_host: np.ndarray, l: int, alphabet: str):
+    from . import _capi
+    keys_host = np.ascontiguousarray(keys_host, dtype=np.uint64)
+    k = keys_host.shape[0]
+    buf = ctypes.create_string_buffer(k * l + 1)
+    _capi.lib().pms8g_decode_keys(keys_host.ctypes.data, k, l, alphabet.encode(), buf)
+    raw = buf.raw[: k * l].decode()
+    return [raw[i * l:(i + 1) * l] for i in range(k)]
+
+
+class _DeviceKeys:
+    """__cuda_array_interface__ view of the library's device key buffer."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (count, 2), "typestr": "<i8", "data": (ptr, True), "version": 3,
+                                         "strides": None}
+
+
+def device_keys_tensor(ptr: int, count: int):
+    import torch
+    if count == 0:
+        return torch.empty((0, 2), dtype=torch.int64, device="cuda")
+    return torch.as_tensor(_DeviceKeys(ptr, count), device="cuda")
+
+
+def run_sharded(problem, config=None, options=None, report=None, group=None):
+    """run_parallel across the ranks of torch.distributed: each rank searches
+    its shard on its GPU, then allgather + device merge; every rank returns
+    the full motif set."""
+    import torch
+    import torch.distributed as dist
+    from . import Context, ParallelOptions, RunReport, _validated
+    import dataclasses
+    options = options or ParallelOptions()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    codes = _validated(problem)
+    n, m = codes.shape
+    opts = dataclasses.replace(options, shard_rank=rank, shard_count=world,
+                               device=options.device if options.device >= 0 else torch.cuda.current_device())
+    ctx = Context(n, m, problem.motif_length, problem.max_mismatches, problem.alphabet, config, opts)
+    try:
+        ctx.load_codes(codes.ctypes.data, False)
+        ctx.run()
+        local_report = RunReport()
+        ctx.result(local_report)
+        ptr, cnt = ctx.keys()
+        local = device_keys_tensor(ptr, cnt).clone()
+        allk = allgather_keys(local, group)
+        merged = merge_keys_device(allk)
+        motifs = decode_keys(merged.cpu().numpy().view(np.uint64), problem.motif_length, problem.alphabet.symbols)
+        if report is not None:
+            report.__dict__.update(local_report.__dict__)
+            report.motif_count = len(motifs)
+            report.gpus = world
+        return motifs
+    finally:
+        ctx.close()
