@@ -1,0 +1,219 @@
+// pms8g — drop-in CLI for `pms8 solve` / `pms8 generate` (tools/pms8.cpp).
+//
+//   pms8g solve <input> [-l L] [-d D] [--alphabet A] [--workers N] [--threshold T]
+//               [--max-motifs K] [--format text|json] [--prune none|pairs|full]
+//               [--no-sort-rows] [--no-pair-matrix] [--reverify] [--device N]
+//   pms8g generate -l L -d D [-n N] [-m M] [--alphabet A] [--seed S]
+//               [--mutation atmost|exact] [-o FILE]
+//
+// stdout/stderr/exit codes follow cmd_solve (tools/pms8.cpp:150-184): one motif
+// per line (or JSON {motifs, report}), a one-line summary on stderr, exit 0 if
+// at least one motif, 1 if none, 2 on usage/input error (:386-389). CLI11 and
+// nlohmann::json are not available here, so argv parsing and JSON are hand-rolled.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <iostream>
+#include <optional>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "pms8g.hpp"
+
+namespace {
+
+struct Usage : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+std::string json_escape(const std::string& s) {
+    std::string o;
+    for (char c : s) {
+        if (c == '"' || c == '\\') o += '\\';
+        o += c;
+    }
+    return o;
+}
+
+int to_int(const std::string& flag, const std::string& v) {
+    try {
+        size_t pos = 0;
+        const int x = std::stoi(v, &pos);
+        if (pos != v.size()) throw std::invalid_argument(v);
+        return x;
+    } catch (...) {
+        throw Usage(flag + ": expected an integer, got '" + v + "'");
+    }
+}
+
+int cmd_solve(const std::vector<std::string>& args, const std::string& command) {
+    std::string input, alphabet, format = "text", prune = "full";
+    std::optional<int> l, d, threshold, workers;
+    std::optional<int64_t> max_motifs;
+    bool no_sort = false, no_pair = false, reverify = false;
+    int device = -1;
+    for (size_t i = 0; i < args.size(); ++i) {
+        const std::string& a = args[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= args.size()) throw Usage(a + " needs a value");
+            return args[++i];
+        };
+        if (a == "-l") l = to_int(a, val());
+        else if (a == "-d") d = to_int(a, val());
+        else if (a == "--alphabet") alphabet = val();
+        else if (a == "--workers") workers = to_int(a, val());
+        else if (a == "--threshold") threshold = to_int(a, val());
+        else if (a == "--max-motifs") max_motifs = to_int(a, val());
+        else if (a == "--format") {
+            format = val();
+            if (format != "text" && format != "json") throw Usage("--format: text or json");
+        } else if (a == "--prune") {
+            prune = val();
+            if (prune != "none" && prune != "pairs" && prune != "full") throw Usage("--prune: none, pairs or full");
+        } else if (a == "--no-sort-rows") no_sort = true;
+        else if (a == "--no-pair-matrix") no_pair = true;
+        else if (a == "--reverify") reverify = true;
+        else if (a == "--device") device = to_int(a, val());
+        else if (!a.empty() && a[0] == '-') throw Usage("unknown option " + a);
+        else if (input.empty()) input = a;
+        else throw Usage("unexpected argument " + a);
+    }
+    if (input.empty()) throw Usage("solve: input file required");
+    if (workers && *workers < 1) throw std::invalid_argument("worker count must be >= 1");
+    const pms8g::SequenceFile file = pms8g::read_sequences(input);
+    auto meta_int = [&](const char* key) -> std::optional<int> {
+        auto it = file.metadata.find(key);
+        if (it == file.metadata.end()) return std::nullopt;
+        return std::stoi(it->second);
+    };
+    if (!l) l = meta_int("l");
+    if (!d) d = meta_int("d");
+    if (!l || !d) {
+        std::cerr << "error: -l and -d are required (no l/d metadata in " << input << ")\n";
+        return 2;
+    }
+    if (alphabet.empty()) {
+        auto it = file.metadata.find("alphabet");
+        alphabet = it != file.metadata.end() ? it->second : "dna";
+    }
+    pms8g::Problem problem;
+    problem.sequences = file.sequences;
+    problem.motif_length = *l;
+    problem.max_mismatches = *d;
+    problem.alphabet = pms8g::alphabet_symbols(alphabet);
+    problem.alphabet_name = alphabet;
+    problem.validate();
+
+    pms8g::SolverConfig config;
+    config.threshold_override = threshold;
+    config.sort_rows = !no_sort;
+    config.use_pair_matrix = !no_pair;
+    config.max_motifs = max_motifs;
+    config.reverify_against_originals = reverify;
+    config.prune_level = prune == "none" ? pms8g::PruneLevel::none
+                         : prune == "pairs" ? pms8g::PruneLevel::pairs
+                                            : pms8g::PruneLevel::full;
+    pms8g::GpuOptions gpu;
+    gpu.device = device;
+    pms8g::RunReport report;
+    const pms8g::MotifSet motifs = pms8g::run_parallel(problem, config, gpu, &report);
+    report.command = command;
+    if (format == "json") {
+        std::ostringstream o;
+        o << "{\n  \"motifs\": [";
+        for (size_t i = 0; i < motifs.size(); ++i) o << (i ? ", " : "") << "\"" << motifs[i] << "\"";
+        o << "],\n  \"report\": {\"n\": " << report.n << ", \"m\": " << report.m << ", \"l\": " << report.l
+          << ", \"d\": " << report.d << ", \"alphabet\": \"" << json_escape(report.alphabet)
+          << "\", \"threshold\": " << report.threshold << ", \"workers\": " << report.workers
+          << ", \"subproblems\": " << report.subproblems << ", \"motif_count\": " << report.motif_count
+          << ", \"wall_seconds\": " << report.wall_seconds << ", \"sample_seconds\": " << report.sample_seconds
+          << ", \"pattern_seconds\": " << report.pattern_seconds << ", \"device_seconds\": " << report.device_seconds
+          << ", \"memory\": {\"device_bytes\": " << report.device_bytes << "}"
+          << ", \"counters\": {\"stacks_explored\": " << report.counters.stacks_explored
+          << ", \"neighborhoods\": " << report.counters.neighborhoods
+          << ", \"neighbors_visited\": " << report.counters.neighbors_visited
+          << ", \"motifs_emitted\": " << report.counters.motifs_emitted
+          << ", \"filter_slots\": " << report.filter_slots << ", \"verify_compares\": " << report.verify_compares
+          << ", \"enum_nodes\": " << report.enum_nodes << "}, \"command\": \"" << json_escape(report.command)
+          << "\"}\n}";
+        std::cout << o.str() << "\n";
+    } else {
+        for (const auto& m : motifs) std::cout << m << "\n";
+        std::cerr << "motifs=" << motifs.size() << " threshold=" << report.threshold << " workers=" << report.workers
+                  << " wall=" << report.wall_seconds << "s"
+                  << " sample=" << report.sample_seconds << "s pattern=" << report.pattern_seconds << "s\n";
+    }
+    return motifs.empty() ? 1 : 0;
+}
+
+int cmd_generate(const std::vector<std::string>& args) {
+    int l = -1, d = -1, n = 20, m = 600;
+    std::string alphabet = "dna", mutation = "atmost", output = "instance.fa";
+    uint64_t seed = 0;
+    for (size_t i = 0; i < args.size(); ++i) {
+        const std::string& a = args[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= args.size()) throw Usage(a + " needs a value");
+            return args[++i];
+        };
+        if (a == "-l") l = to_int(a, val());
+        else if (a == "-d") d = to_int(a, val());
+        else if (a == "-n") n = to_int(a, val());
+        else if (a == "-m") m = to_int(a, val());
+        else if (a == "--alphabet") alphabet = val();
+        else if (a == "--seed") seed = std::strtoull(val().c_str(), nullptr, 10);
+        else if (a == "--mutation") {
+            mutation = val();
+            if (mutation != "atmost" && mutation != "exact") throw Usage("--mutation: atmost or exact");
+        } else if (a == "-o" || a == "--output") output = val();
+        else throw Usage("unknown option " + a);
+    }
+    if (l < 0 || d < 0) throw Usage("generate: -l and -d are required");
+    const std::string sym = pms8g::alphabet_symbols(alphabet);
+    std::vector<uint8_t> codes(static_cast<size_t>(n) * m), motif(l > 0 ? l : 1);
+    std::vector<int32_t> pos(n > 0 ? n : 1);
+    if (pms8g_generate(n, m, l, d, static_cast<int>(sym.size()), seed, mutation == "exact", codes.data(),
+                       motif.data(), pos.data()) != PMS8G_OK)
+        throw std::invalid_argument("need 1 <= l <= m, 0 <= d <= l, n >= 1");
+    std::vector<std::string> seqs(n), names(n);
+    std::string motif_s(l, ' '), positions;
+    for (int p = 0; p < l; ++p) motif_s[p] = sym[motif[p]];
+    for (int i = 0; i < n; ++i) {
+        seqs[i].resize(m);
+        for (int j = 0; j < m; ++j) seqs[i][j] = sym[codes[static_cast<size_t>(i) * m + j]];
+        names[i] = "seq_" + std::to_string(i) + " pos=" + std::to_string(pos[i]);
+        positions += (i ? "," : "") + std::to_string(pos[i]);
+    }
+    // metadata lines as cmd_generate writes them (tools/pms8.cpp:82-97)
+    std::vector<std::pair<std::string, std::string>> meta{
+        {"format", "pms8-planted-instance-v1"}, {"n", std::to_string(n)}, {"m", std::to_string(m)},
+        {"l", std::to_string(l)}, {"d", std::to_string(d)}, {"alphabet", alphabet},
+        {"seed", std::to_string(seed)}, {"mutation", mutation}, {"motif", motif_s}, {"positions", positions}};
+    pms8g::write_fasta(output, names, seqs, meta);
+    std::cout << motif_s << "\n";
+    std::cerr << "wrote " << output << " (" << n << " sequences of length " << m << ")\n";
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    std::vector<std::string> args(argv + 1, argv + argc);
+    std::string command;
+    for (int i = 0; i < argc; ++i) command += (i ? " " : "") + std::string(argv[i]);
+    try {
+        if (args.empty()) throw Usage("a subcommand is required: solve | generate");
+        const std::string sub = args[0];
+        args.erase(args.begin());
+        if (sub == "solve") return cmd_solve(args, command);
+        if (sub == "generate") return cmd_generate(args);
+        throw Usage("unknown subcommand " + sub);
+    } catch (const Usage& e) {
+        std::cerr << "usage error: " << e.what() << "\n";
+        return 2;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 2;
+    }
+}

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (tests/golden/, produced by oracle/_ref) and the C oracle. Integer work:
+every comparison is exact (bit-identical sorted motif lists)."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import _oracle as O
+import paper_1307_0571_b200 as P
+from conftest import ROOT, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def planted(l, d, seed, n=20, m=600):
+    return P.generate_planted_instance(
+        P.PlantedInstanceSpec(n=n, m=m, l=l, d=d, seed=seed, mutation=P.MutationMode.exactly_d))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_planted_13_4_full_instance(seed):
+    g = [x for x in golden("planted_13_4.json") if x["seed"] == seed][0]
+    inst = planted(13, 4, seed)
+    rep = P.RunReport()
+    t = g["report"]["threshold"]
+    got = P.solve(inst.problem, P.SolverConfig(threshold_override=t), rep)
+    assert got == g["motifs"]
+    assert inst.motif in got
+    # at the reference's threshold the GPU explores the identical tree
+    assert rep.counters.stacks_explored == g["report"]["stacks_explored"]
+    assert rep.counters.neighborhoods == g["report"]["neighborhoods"]
+    assert rep.counters.neighbors_visited == g["report"]["neighbors_visited"]
+    assert rep.counters.motifs_emitted == g["report"]["motifs_emitted"]
+    assert rep.subproblems == 588
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_planted_17_6_full_instance(seed):
+    g = [x for x in golden("planted_17_6.json") if x["seed"] == seed][0]
+    inst = planted(17, 6, seed)
+    got = P.solve(inst.problem)
+    assert got == g["motifs"]
+    assert inst.motif in got
+    assert all(O.is_motif(inst.codes, 17, 6, mo) for mo in got)
+
+
+def _anchor_parity(name, l, d):
+    path = os.path.join(ROOT, "tests", "golden", name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    g = golden(name)
+    inst = planted(l, d, g["seed"])
+    for a in g["anchors"]:
+        got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=[a["offset"]]))
+        assert got == a["motifs"], a["offset"]
+
+
+def test_anchor_sample_21_8():
+    _anchor_parity("anchors_21_8.json", 21, 8)
+
+
+def test_anchor_sample_23_9():
+    _anchor_parity("anchors_23_9.json", 23, 9)
+
+
+def test_small_random_and_edge_cases():
+    for case in golden("small_random.json"):
+        prob = P.Problem(case["sequences"], case["l"], case["d"])
+        cfg = P.SolverConfig(threshold_override=case["t"] or None)
+        assert P.solve(prob, cfg) == case["motifs"], case
+
+
+def test_threshold_invariance():
+    g = golden("planted_13_4.json")[0]
+    inst = planted(13, 4, 1)
+    for t in (1, 2, 3, 4, 5, 6, 20):
+        assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == g["motifs"], t
+
+
+def test_prune_levels_and_row_order_do_not_change_output():
+    codes, _, _ = O.generate(8, 2, 11, n=6, m=50)
+    seqs = ["".join("ACGT"[c] for c in row) for row in codes]
+    want = O.brute_force(codes, 8, 2)
+    prob = P.Problem(seqs, 8, 2)
+    for lvl in (P.PruneLevel.none, P.PruneLevel.pairs, P.PruneLevel.full):
+        for sort_rows in (True, False):
+            for t in (1, 2, 3):
+                cfg = P.SolverConfig(prune_level=lvl, sort_rows=sort_rows, threshold_override=t)
+                assert P.solve(prob, cfg) == want, (lvl, sort_rows, t)
+
+
+def test_random_instances_vs_oracle():
+    rng = np.random.default_rng(5)
+    for _ in range(25):
+        n = int(rng.integers(2, 9))
+        l = int(rng.integers(5, 12))
+        m = int(rng.integers(l, 60))
+        d = int(rng.integers(0, 4))
+        codes = rng.integers(0, 4, (n, m)).astype(np.uint8)
+        seqs = ["".join("ACGT"[c] for c in row) for row in codes]
+        want, _ = O.solve(codes, l, d)
+        assert P.solve(P.Problem(seqs, l, d)) == want, (n, m, l, d)
+
+
+def test_long_motifs_two_word_path():
+    # l > 32 exercises the two-word bit planes (W=2); small n keeps it fast
+    for l, d, seed in [(33, 3, 1), (40, 5, 2), (50, 8, 3), (64, 10, 4)]:
+        inst = planted(l, d, seed, n=5, m=90)
+        want, _ = O.solve(inst.codes, l, d)
+        got = P.solve(inst.problem)
+        assert got == want, (l, d)
+        assert inst.motif in got
+
+
+def test_reverify_and_caps():
+    inst = planted(13, 4, 1)
+    g = golden("planted_13_4.json")[0]
+    assert P.solve(inst.problem, P.SolverConfig(reverify_against_originals=True)) == g["motifs"]
+    with pytest.raises(P.SolverRuntimeError, match="motif cap of 3 exceeded"):
+        P.solve(inst.problem, P.SolverConfig(max_motifs=3))
+    assert P.solve(inst.problem, P.SolverConfig(max_motifs=100)) == g["motifs"]
+
+
+def test_invalid_arguments():
+    inst = planted(13, 4, 1)
+    with pytest.raises(P.InvalidArgument, match=r"threshold must be in \[1, n\]"):
+        P.solve(inst.problem, P.SolverConfig(threshold_override=21))
+    with pytest.raises(P.InvalidArgument, match=r"threshold must be in \[1, n\]"):
+        P.solve(inst.problem, P.SolverConfig(threshold_override=0))
+    with pytest.raises(P.InvalidArgument, match="anchor offset"):
+        P.run_parallel(inst.problem, None, P.ParallelOptions(anchors=[588]))
+
+
+def test_shards_union_to_full_answer():
+    g = [x for x in golden("planted_13_4.json") if x["seed"] == 3][0]
+    inst = planted(13, 4, 3)
+    union = set()
+    for r in range(3):
+        union |= set(P.run_parallel(inst.problem, None, P.ParallelOptions(shard_rank=r, shard_count=3)))
+    assert sorted(union) == g["motifs"]
+
+
+def test_device_merge_keys():
+    import torch
+    from paper_1307_0571_b200.parallel import merge_keys_device
+    rng = np.random.default_rng(2)
+    k = rng.integers(0, 1 << 40, (5000, 2)).astype(np.int64)
+    k[:, 1] = rng.integers(0, 3, 5000)
+    k = np.concatenate([k, k[:1000]])
+    got = merge_keys_device(torch.as_tensor(k, device="cuda")).cpu().numpy()
+    want = np.unique(k.view(np.uint64)[:, ::-1], axis=0)[:, ::-1].view(np.int64)
+    assert (got == want).all()
+
+
+def test_device_resident_context_matches():
+    import torch
+    g = golden("planted_13_4.json")[0]
+    inst = planted(13, 4, 1)
+    ctx = P.Context(20, 600, 13, 4)
+    dev = torch.as_tensor(inst.codes, device="cuda").contiguous()
+    torch.cuda.synchronize()
+    ctx.load_codes(dev.data_ptr(), True)
+    for _ in range(2):
+        ctx.run()
+        assert ctx.result() == g["motifs"]
+    ctx.close()
+
+
+def test_cli_solve_matches_reference_stdout(tmp_path):
+    exe = os.path.join(ROOT, "paper_1307_0571_b200", "bin", "pms8g")
+    f = tmp_path / "i.fa"
+    subprocess.run([exe, "generate", "-l", "13", "-d", "4", "--seed", "1", "--mutation", "exact", "-o", str(f)],
+                   check=True, capture_output=True)
+    r = subprocess.run([exe, "solve", str(f)], capture_output=True, text=True)
+    assert r.returncode == 0
+    assert r.stdout.split() == golden("planted_13_4.json")[0]["motifs"]
+    assert r.stderr.startswith("motifs=9 threshold=")
+    r = subprocess.run([exe, "solve", str(f), "--format", "json"], capture_output=True, text=True)
+    assert json.loads(r.stdout)["motifs"] == golden("planted_13_4.json")[0]["motifs"]
+    # no motif -> exit 1 (tools/pms8.cpp:183)
+    g = tmp_path / "none.txt"
+    g.write_text("AAAAAAAA\nCCCCCCCC\n")
+    r = subprocess.run([exe, "solve", str(g), "-l", "8", "-d", "0"], capture_output=True, text=True)
+    assert r.returncode == 1 and r.stdout == ""
