@@ -112,6 +112,9 @@ int pms8g_ctx_result(pms8g_ctx* ctx, pms8g_result* out, char* err, size_t errlen
 void* pms8g_ctx_stream(pms8g_ctx* ctx); /* cudaStream_t */
 /* Dedicated event pair around the main search kernel of the last launch. */
 int pms8g_ctx_kernel_ms(pms8g_ctx* ctx, float* search_ms, float* rowbuild_ms);
+/* Raw device counters of the last run (diagnostics: per-rule rejections, task
+ * duration histogram); returns the number of counters available. */
+int pms8g_ctx_counters(pms8g_ctx* ctx, uint64_t* out, int cap);
 void pms8g_ctx_destroy(pms8g_ctx* ctx);
 
 /* Device sort+unique of `count` keys (2 x uint64 each) at dev_in into dev_out

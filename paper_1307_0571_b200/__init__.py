@@ -449,6 +449,12 @@ class Context:
         _capi.lib().pms8g_ctx_keys(self._ptr, ctypes.byref(p), ctypes.byref(c))
         return int(p.value or 0), int(c.value)
 
+    def counters(self):
+        """Raw device counters of the last run (see pms8g_device.cuh Ctr)."""
+        buf = (ctypes.c_uint64 * 64)()
+        k = _capi.lib().pms8g_ctx_counters(self._ptr, buf, 64)
+        return [int(buf[i]) for i in range(min(k, 64))]
+
     def kernel_ms(self):
         a, b = ctypes.c_float(), ctypes.c_float()
         _capi.lib().pms8g_ctx_kernel_ms(self._ptr, ctypes.byref(a), ctypes.byref(b))

@@ -64,6 +64,7 @@ class Result(ctypes.Structure):
 EXPORTS = [
     "pms8g_default_options", "pms8g_solve", "pms8g_result_free", "pms8g_ctx_create", "pms8g_ctx_load_codes",
     "pms8g_ctx_run", "pms8g_ctx_keys", "pms8g_ctx_result", "pms8g_ctx_stream", "pms8g_ctx_kernel_ms",
+    "pms8g_ctx_counters",
     "pms8g_ctx_destroy", "pms8g_merge_keys", "pms8g_decode_keys", "pms8g_generate", "pms8g_estimate_threshold",
     "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version",
 ]
@@ -104,6 +105,8 @@ def lib():
     L.pms8g_ctx_stream.restype = c_vp
     L.pms8g_ctx_kernel_ms.argtypes = [c_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     L.pms8g_ctx_kernel_ms.restype = c_int
+    L.pms8g_ctx_counters.argtypes = [c_vp, ctypes.POINTER(ctypes.c_uint64), c_int]
+    L.pms8g_ctx_counters.restype = c_int
     L.pms8g_ctx_destroy.argtypes = [c_vp]
     L.pms8g_ctx_destroy.restype = None
     L.pms8g_merge_keys.argtypes = [c_vp, c_i64, c_vp, ctypes.POINTER(c_i64), c_vp, c_char_p, c_sz]

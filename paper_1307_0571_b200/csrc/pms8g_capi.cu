@@ -104,6 +104,11 @@ struct pms8g_ctx {
     int* h_err = nullptr;
     int blocks = 0, warps = 0;
     size_t smem = 0;
+    WarpPlan plan{};
+    QueueState* d_qs = nullptr;
+    unsigned int* d_qstate = nullptr;
+    uint8_t* d_qslots = nullptr;
+    int qcap = 0, qslot_bytes = 0;
     size_t device_bytes = 0;
     long long unique_count = 0;
     pms8g_report report{};
@@ -351,20 +356,21 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     // launch shape: one persistent block per SM, as many warps as the
     // shared-memory l-mer table leaves room for
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    c->plan = make_plan(c->W, l, t);
     int warps = opt.warps_per_block > 0 ? opt.warps_per_block : 16;
-    while (warps > 1 && search_smem(c->W, c->K, warps) > smem_cap) --warps;
-    if (search_smem(c->W, c->K, warps) > smem_cap)
+    while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) > smem_cap) --warps;
+    if (search_smem(c->W, c->K, warps, c->plan) > smem_cap)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
                                  "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K, smem_cap));
     c->warps = warps;
-    c->smem = search_smem(c->W, c->K, warps);
+    c->smem = search_smem(c->W, c->K, warps, c->plan);
     c->blocks = c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
-    if (set_search_smem(c->W, c->smem) != cudaSuccess)
+    if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
 
     const int na = static_cast<int>(c->anchors.size());
     c->level_cap = c->K;
-    c->node_cap = 32 * (l + 2);
+    c->node_cap = 64 * (l + 4);
     const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
     const size_t node_words = static_cast<size_t>(c->node_cap) * node_bytes(c->W) / 4;
     c->scratch_words = (lvl_words + node_words + 31) / 32 * 32;
@@ -385,6 +391,12 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     AL(c->d_unique_count, sizeof(long long));
     AL(c->d_counters, sizeof(unsigned long long) * C_NCTR);
     AL(c->d_err, sizeof(int));
+    c->qcap = 8192;
+    if (const char* q = std::getenv("PMS8G_QCAP")) c->qcap = std::max(16, std::atoi(q));  // ring stress tests
+    c->qslot_bytes = static_cast<int>(task_slot_bytes(c->W));
+    AL(c->d_qs, sizeof(QueueState));
+    AL(c->d_qslots, static_cast<size_t>(c->qcap) * c->qslot_bytes);
+    AL(c->d_qstate, sizeof(unsigned int) * c->qcap);
     AL(c->d_fail, sizeof(int));
 #undef AL
     if (cudaMallocHost(reinterpret_cast<void**>(&c->h_counters), sizeof(unsigned long long) * (C_NCTR + 2)) !=
@@ -406,7 +418,7 @@ void pms8g_ctx_destroy(pms8g_ctx* c) {
     void* ptrs[] = {c->d_codes, c->d_table,      c->d_anchors,     c->d_l1,           c->d_meta,
                     c->d_task_base, c->d_task_counter, c->d_scratch, c->d_keys,   c->d_keys_sorted,
                     c->d_keys_unique, c->d_key_count, c->d_unique_count, c->d_cub, c->d_counters,
-                    c->d_err,     c->d_fail};
+                    c->d_err,     c->d_fail, c->d_qs, c->d_qslots, c->d_qstate};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -439,6 +451,12 @@ int pms8g_ctx_keys(pms8g_ctx* c, const uint64_t** dev_keys, int64_t* count) {
     *dev_keys = reinterpret_cast<const uint64_t*>(c->d_keys_unique);
     *count = c->unique_count;
     return PMS8G_OK;
+}
+
+int pms8g_ctx_counters(pms8g_ctx* c, uint64_t* out, int cap) {
+    const int k = cap < C_NCTR ? cap : C_NCTR;
+    for (int i = 0; i < k; ++i) out[i] = c->h_counters[i];
+    return C_NCTR;
 }
 
 int pms8g_ctx_kernel_ms(pms8g_ctx* c, float* search_ms, float* rowbuild_ms) {
@@ -619,7 +637,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
     for (int attempt = 0; attempt < 8; ++attempt) {
         CU(cudaMemsetAsync(c->d_counters, 0, sizeof(unsigned long long) * C_NCTR, s));
         CU(cudaMemsetAsync(c->d_key_count, 0, sizeof(unsigned long long), s));
-        CU(cudaMemsetAsync(c->d_task_counter, 0, sizeof(unsigned long long), s));
+        CU(cudaMemsetAsync(c->d_qs, 0, sizeof(QueueState), s));
+        CU(cudaMemsetAsync(c->d_qstate, 0, sizeof(unsigned int) * c->qcap, s));
         CU(cudaMemsetAsync(c->d_err, 0, sizeof(int), s));
         CU(cudaMemsetAsync(c->d_fail, 0, sizeof(int), s));
         CU(launch_encode(c->W, c->d_codes, c->n, c->m, c->l, c->w, c->d_table, c->d_err, s));
@@ -644,7 +663,13 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.anchor_off = c->d_anchors;
         P.task_base = c->d_task_base;
         P.nanchors = na;
-        P.task_counter = c->d_task_counter;
+        P.qs = c->d_qs;
+        P.qslots = c->d_qslots;
+        P.qstate = c->d_qstate;
+        P.qcap = c->qcap;
+        P.qslot_bytes = c->qslot_bytes;
+        P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
+        P.plan = c->plan;
         P.scratch = c->d_scratch;
         P.scratch_words = c->scratch_words;
         P.level_cap = c->level_cap;
@@ -668,6 +693,10 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         if (c->h_err[0] & 2)
             return fail(err, errlen, PMS8G_ERR_RUNTIME, "enumeration stack overflow (l=%d, capacity %d nodes)", c->l,
                         c->node_cap);
+        if (c->h_err[0] & 8)
+            return fail(err, errlen, PMS8G_ERR_RUNTIME, "search work queue watchdog fired (no progress)");
+        if (c->h_err[0] & 4)
+            return fail(err, errlen, PMS8G_ERR_LOGIC, "replay of a donated task diverged from its donor");
         const long long raw = static_cast<long long>(c->h_counters[C_NCTR]);
         if (c->opt.max_motifs >= 0 && raw > c->opt.max_motifs)
             return fail(err, errlen, PMS8G_ERR_RUNTIME, "motif cap of %lld exceeded",

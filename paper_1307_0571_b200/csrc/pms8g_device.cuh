@@ -44,7 +44,50 @@ enum Ctr {
     C_NODES,
     C_CLK_FILTER,
     C_CLK_PATTERN,
-    C_NCTR
+    C_PAIR_REJ,   // slots rejected by the pair rule
+    C_TRI_REJ,    // slots rejected by the Theorem-1 triple rule
+    C_TASKS,      // tasks processed
+    C_DONATED,    // dynamic tasks donated
+    C_REPLAYS,    // filter pushes replayed by receivers of donated tasks
+    C_HIST0,      // task duration histogram: C_HIST0 + floor(log2(cycles)), 40 buckets
+    C_NCTR = C_HIST0 + 40
+};
+
+constexpr int NDON = 32;  // enumeration nodes per donated task
+
+// Global work-queue state (zeroed per run). Static tasks are the (S1 l-mer,
+// depth-1 branch) pairs indexed through task_base; dynamic tasks are
+// donated by busy warps while other warps wait.
+struct QueueState {
+    unsigned long long static_next;  // next static task
+    unsigned long long head;         // next dynamic slot to consume
+    unsigned long long alloc;        // dynamic slots reserved by producers
+    unsigned long long ready_unused;
+    unsigned int busy;               // warps holding a task
+    unsigned int waiting;            // warps idle, waiting for work
+    unsigned long long pad[4];
+};
+
+// Dynamic task slot header; kind 1 slots are followed by the donated nodes.
+struct TaskHeader {
+    int32_t anchor;  // anchor index
+    int16_t kind;    // 0: branch range [a0, a1) at level k; 1: a0 enumeration nodes of the k-tuple
+    int16_t k;
+    int32_t a0, a1;
+    uint32_t stack[MAXT];
+    uint32_t pad[2];
+};
+
+// Per-warp shared-memory plan (byte offsets inside the warp's region),
+// computed on the host from (W, l, t).
+struct WarpPlan {
+    int bytes;
+    int off_thr;    // uint8 [(l+1) * (npair(t) + ntri(t))]
+    int off_cand;   // Lmer<W> [cand_cap]
+    int off_nodes;  // Node<W> [node_smem]
+    int cand_cap;
+    int node_smem;
+    int npair, ntri;
 };
 
 struct SearchParams {
@@ -55,11 +98,16 @@ struct SearchParams {
     const int32_t* anchor_off;    // [nanchors]
     const long long* task_base;   // [nanchors + 1]
     int nanchors;
-    unsigned long long* task_counter;
+    QueueState* qs;
+    uint8_t* qslots;              // [qcap][qslot_bytes]
+    unsigned int* qstate;         // [qcap] slot round state (2r free, 2r+1 published)
+    int qcap, qslot_bytes;
+    int donate;                   // 1: donate work to idle warps
     uint32_t* scratch;            // per-warp level storage + node stack
     size_t scratch_words;         // uint32 words per warp
     int level_cap;                // entries per level buffer
-    int node_cap;                 // nodes per warp stack
+    int node_cap;                 // nodes per warp stack (global part)
+    WarpPlan plan;
     unsigned long long* keys;     // 2 x u64 per motif key {lo, hi}
     unsigned long long* key_count;
     long long key_cap;

@@ -11,8 +11,9 @@ namespace pms8g {
 
 size_t lmer_bytes(int W);
 size_t node_bytes(int W);
-size_t search_smem(int W, int K, int warps);
-size_t search_warp_smem(int W);
+WarpPlan make_plan(int W, int l, int t);
+size_t search_smem(int W, int K, int warps, const WarpPlan& plan);
+size_t task_slot_bytes(int W);
 
 cudaError_t launch_encode(int W, const uint8_t* codes, int n, int m, int l, int w, void* table, int* err,
                           cudaStream_t s);
@@ -20,7 +21,7 @@ cudaError_t launch_rowbuild(int W, const void* table, int n, int w, int d, int K
                             const int32_t* anchor_off, int nanchors, uint32_t* l1_entries, LevelMeta* l1_meta,
                             unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_taskscan(const LevelMeta* l1_meta, int nanchors, int t, long long* task_base, cudaStream_t s);
-cudaError_t set_search_smem(int W, size_t bytes);
+cudaError_t set_search_smem(int W, int t, size_t bytes);
 cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s);
 cudaError_t launch_reverify(int W, const void* table, int n, int w, int l, int d, const unsigned long long* keys,
                             long long count, int* fail, cudaStream_t s);

@@ -1,0 +1,983 @@
+// pms8g_search.cu — K4: the persistent sm_100a search kernel.
+//
+// One warp = one depth-first worker. Work arrives as tasks:
+//   static  (S1 l-mer a, depth-1 branch j): push the j-th l-mer u of a's
+//           branching row, then search below it (run_anchored + recurse,
+//           src/solver.cpp:406-432, with the first level unrolled);
+//   dynamic (a, stack prefix, branch range at level k) or (a, k-tuple, DFS
+//           nodes): donated by a busy warp while other warps wait, rebuilt by
+//           the receiver by replaying the prefix pushes.
+// Per push, the warp filters every remaining row with the pair rule and
+// PMS8's Theorem-1 triple rule (MotifSearch::push, src/solver.cpp:245-337).
+// At the switch depth t it enumerates the tuple's common d-neighbourhood
+// (NeighborhoodEnumerator, src/neighborhood.cpp:164-270) 16 nodes x 4
+// symbols per round and verifies candidates breadth-first against the
+// remaining rows (verify_candidate, src/solver.cpp:344-362), smallest row
+// first, compacting survivors between rows.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pms8g_common.cuh"
+#include "pms8g_device.cuh"
+#include "pms8g_launch.h"
+
+namespace pms8g {
+
+using namespace dev;
+
+namespace {
+
+template <int W>
+struct Node {
+    Lmer<W> c;    // candidate prefix planes
+    uint32_t rA;  // budgets of members 0..3, biased by +64, one byte each
+    uint32_t rB;  // budgets of members 4..5 (bytes 0,1); prefix length p in byte 3
+};
+
+template <int W>
+struct NodeSmem {
+    static constexpr int N = W == 1 ? 128 : 64;  // power of two
+};
+
+struct WarpFixed {
+    LevelMeta lev[MAXT + 1];
+    int iter[MAXT + 1];
+    int iter_end[MAXT + 1];
+    uint32_t stack_id[MAXT];
+    uint16_t cnt_by_row[MAXN];
+    uint8_t vorder[MAXN];
+    uint32_t eq[64];
+    uint8_t cons[68];
+    TaskHeader task;
+    unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
+};
+
+enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
+            W_DONATED, W_REPLAYS, W_CLKF, W_CLKP, W_N };
+
+constexpr int MAXCH = 5;  // candidate chunks of 32 held in registers by verify
+
+template <int W, int MT>
+struct WarpCtx {
+    const SearchParams* P;
+    const Lmer<W>* T;  // l-mer table in shared memory
+    WarpFixed* S;
+    uint8_t* thr;      // per-tuple suffix thresholds
+    Lmer<W>* cand;     // candidate buffer
+    Node<W>* node_smem;
+    Node<W>* node_glob;
+    uint32_t* lvl_glob;
+    const uint32_t* l1;  // level-1 entries of the current anchor
+    int anchor;          // anchor index of the current task
+    int lane;
+    int pushes_since_check;
+    __device__ __forceinline__ void add(int i, unsigned long long v) {
+        if (lane == 0) S->ctr[i] += v;
+    }
+};
+
+template <int W, int MT>
+__device__ __forceinline__ uint32_t* level_entries(WarpCtx<W, MT>& C, int k) {
+    return k == 1 ? const_cast<uint32_t*>(C.l1) : C.lvl_glob + static_cast<size_t>(k - 2) * C.P->level_cap;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
+    return *reinterpret_cast<const volatile unsigned int*>(p);
+}
+
+// ---------------------------------------------------------------- push filter
+// Push of u = stack[k] onto a stack of k members: filter level k (minus its
+// branching row) into level k+1. Returns viable (no remaining row emptied).
+template <int W, int MT>
+__device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane;
+    WarpFixed& S = *C.S;
+    LevelMeta& Ls = S.lev[k];
+    LevelMeta& Ld = S.lev[k + 1];
+    const uint32_t* src = level_entries<W, MT>(C, k);
+    uint32_t* dst = level_entries<W, MT>(C, k + 1);
+    const int d = P.d, six_d = 6 * d, two_d = 2 * d;
+    const long long f0 = clock64();
+
+    const Lmer<W> U = C.T[S.stack_id[k] & ID_MASK];
+    Lmer<W> Sm[MT];
+    Mask<W> Miu[MT];
+    int hs[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        if (i < k) {
+            Sm[i] = C.T[S.stack_id[i] & ID_MASK];
+            Miu[i] = mism<W>(Sm[i], U);
+            hs[i] = popcm<W>(Miu[i]);
+        }
+    }
+    const int jb = Ls.branch;
+    const int bstart = Ls.start[jb], bcnt = Ls.cnt[jb];
+    const int n_iter = Ls.total - bcnt;
+    const int nrows = Ls.nrows;
+    if (lane < MAXN) S.cnt_by_row[lane] = 0;
+    __syncwarp();
+    int out = 0;
+    bool dead = false;
+    unsigned pair_rej = 0, tri_rej = 0;
+    for (int base = 0; base < n_iter; base += 32) {
+        const int f = base + lane;
+        const bool valid = f < n_iter;
+        const int idx = f < bstart ? f : f + bcnt;
+        const uint32_t e = valid ? src[idx] : 0xFFFFFFFFu;
+        bool keep = false;
+        if (valid) {
+            const Lmer<W> V = C.T[e & ID_MASK];
+            const Mask<W> mu = mism<W>(V, U);
+            const int hvu = popcm<W>(mu);
+            keep = hvu <= two_d;
+            pair_rej += !keep;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                if (i < k && keep) {
+                    const Mask<W> mi = mism<W>(V, Sm[i]);
+                    const int hvi = popcm<W>(mi);
+                    const int sum = hvi + hvu + hs[i];
+                    if (sum > six_d) {
+                        keep = false;
+                    } else {
+                        const int mn = min(min(hvi, hvu), hs[i]);
+                        if (sum + mn > six_d) keep = sum + popc_and3<W>(mi, mu, Miu[i]) <= six_d;
+                    }
+                    tri_rej += !keep;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
+        out += __popc(bal);
+        // per-row kept counts: rows are contiguous segments of the flat range
+        const uint32_t row = e >> 24;
+        const uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1);
+        const uint32_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        const bool first = valid && (lane == 0 || prow != row);
+        const bool nvalid = (f + 1) < n_iter;
+        const bool last = valid && (lane == 31 || !nvalid || nrow != row);
+        const unsigned starts = __ballot_sync(0xffffffffu, first);
+        bool empty_row = false;
+        if (last) {
+            const int s0 = 31 - __clz(starts & ((2u << lane) - 1u));
+            const unsigned segmask = ((2u << lane) - 1u) & ~((1u << s0) - 1u);
+            const int kept = __popc(bal & segmask) + S.cnt_by_row[row];
+            S.cnt_by_row[row] = static_cast<uint16_t>(kept);
+            const bool complete = (lane < 31 && (!nvalid || nrow != row)) || (lane == 31 && !nvalid);
+            empty_row = complete && kept == 0;
+        }
+        __syncwarp();
+        if (__any_sync(0xffffffffu, empty_row)) {
+            dead = true;
+            break;
+        }
+    }
+    C.add(W_PUSH, 1);
+    C.add(W_SLOTS, static_cast<unsigned long long>(n_iter));
+    {
+        unsigned pr = pair_rej, tr = tri_rej;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            pr += __shfl_xor_sync(0xffffffffu, pr, sh);
+            tr += __shfl_xor_sync(0xffffffffu, tr, sh);
+        }
+        C.add(W_PAIRREJ, pr);
+        C.add(W_TRIREJ, tr);
+    }
+    bool ok = !dead;
+    if (ok) {
+        const int nr2 = nrows - 1;
+        int c = 0;
+        uint8_t row = 0;
+        if (lane < nr2) {
+            const int j = lane < jb ? lane : lane + 1;
+            row = Ls.order[j];
+            c = S.cnt_by_row[row];
+        }
+        int incl = c;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, s);
+            if (lane >= s) incl += v;
+        }
+        if (__any_sync(0xffffffffu, lane < nr2 && c == 0)) {
+            ok = false;
+        } else {
+            int key = lane < nr2 ? (c << 8) | lane : 0x7FFFFFFF;
+            if (P.sort_rows) {
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, s));
+            } else {
+                key = __shfl_sync(0xffffffffu, key, 0);
+            }
+            if (lane < nr2) {
+                Ld.start[lane] = static_cast<uint16_t>(incl - c);
+                Ld.cnt[lane] = static_cast<uint16_t>(c);
+                Ld.order[lane] = row;
+            }
+            if (lane == 0) {
+                Ld.nrows = nr2;
+                Ld.total = out;
+                Ld.branch = key & 0xFF;
+                Ld.viable = 1;
+            }
+            C.add(W_VIABLE, 1);
+        }
+    }
+    __syncwarp();
+    C.add(W_CLKF, static_cast<unsigned long long>(clock64() - f0));
+    return ok;
+}
+
+// ---------------------------------------------------------------- donation
+// Publish one dynamic task (header + nnodes nodes fetched by getnode(i)).
+// Bounded MPMC ring: position s lives in slot s % qcap during round
+// r = s / qcap; the slot state is 2r while free for that round's producer and
+// 2r+1 once published, and the consumer frees it for round r+1 (2r+2) after
+// copying the task out, so a slot is never overwritten while being read.
+template <int W, int MT, typename F>
+__device__ __noinline__ void publish(WarpCtx<W, MT>& C, const TaskHeader& h, int nnodes, F getnode) {
+    const SearchParams& P = *C.P;
+    unsigned long long s = 0;
+    if (C.lane == 0) {
+        s = atomicAdd(&P.qs->alloc, 1ull);
+        const unsigned int want = static_cast<unsigned int>(2 * (s / static_cast<unsigned long long>(P.qcap)));
+        while (ld_volatile(&P.qstate[s % static_cast<unsigned long long>(P.qcap)]) != want) __nanosleep(200);
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
+    const unsigned long long slot_i = s % static_cast<unsigned long long>(P.qcap);
+    uint8_t* slot = P.qslots + slot_i * P.qslot_bytes;
+    const uint32_t* hs = reinterpret_cast<const uint32_t*>(&h);
+    uint32_t* hd = reinterpret_cast<uint32_t*>(slot);
+    for (int x = C.lane; x < static_cast<int>(sizeof(TaskHeader) / 4); x += 32) hd[x] = hs[x];
+    Node<W>* nd = reinterpret_cast<Node<W>*>(slot + sizeof(TaskHeader));
+    for (int x = C.lane; x < nnodes; x += 32) nd[x] = getnode(x);
+    __threadfence();
+    __syncwarp();
+    if (C.lane == 0) {
+        __threadfence();
+        atomicExch(&P.qstate[slot_i], static_cast<unsigned int>(2 * (s / static_cast<unsigned long long>(P.qcap)) + 1));
+    }
+    __syncwarp();
+    C.add(W_DONATED, 1);
+}
+
+// True when idle warps are waiting and the queue cannot feed them.
+template <int W, int MT>
+__device__ bool starving(WarpCtx<W, MT>& C) {
+    const SearchParams& P = *C.P;
+    int want = 0;
+    if (C.lane == 0) {
+        const unsigned int waiting = ld_volatile(&P.qs->waiting);
+        if (waiting > 0) {
+            const unsigned long long alloc = ld_volatile(&P.qs->alloc), head = ld_volatile(&P.qs->head);
+            const unsigned long long queued = alloc > head ? alloc - head : 0;
+            want = queued < waiting;
+        }
+    }
+    return __shfl_sync(0xffffffffu, want, 0) != 0;
+}
+
+// DFS-level donation: give away the upper half of the remaining branch range
+// of the shallowest level in [kmin, k] that has at least two branches left.
+template <int W, int MT>
+__device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k) {
+    if (!C.P->donate) return;
+    if (++C.pushes_since_check < 4) return;
+    C.pushes_since_check = 0;
+    if (!starving<W, MT>(C)) return;
+    WarpFixed& S = *C.S;
+    for (int kk = kmin; kk <= k; ++kk) {
+        const int it = S.iter[kk], end = S.iter_end[kk];
+        if (end - it >= 2) {
+            const int mid = it + (end - it + 1) / 2;
+            TaskHeader h;
+            h.anchor = C.anchor;
+            h.kind = 0;
+            h.k = static_cast<int16_t>(kk);
+            h.a0 = mid;
+            h.a1 = end;
+#pragma unroll
+            for (int i = 0; i < MAXT; ++i) h.stack[i] = i < kk ? S.stack_id[i] : 0u;
+            h.pad[0] = h.pad[1] = 0;
+            __syncwarp();
+            if (C.lane == 0) S.iter_end[kk] = mid;
+            __syncwarp();
+            publish<W, MT>(C, h, 0, [&](int) { return Node<W>{}; });
+            return;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- verification
+// One row pass of the breadth-first verification, specialised on the number
+// of 32-candidate chunks each lane holds in registers: every row entry is
+// loaded once (32 per coalesced load) and broadcast by shuffle, and each
+// compare instruction covers 32 x NCH candidate/entry pairs. Survivors are
+// compacted to the front of the buffer; returns their number.
+template <int W, int NCH>
+__device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const uint32_t* entries, int st, int cnt,
+                                         int n, int d, int lane, int& scanned) {
+    Lmer<W> cd[NCH];
+    bool alive[NCH], hit[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        alive[ch] = ch * 32 + lane < n;
+        hit[ch] = false;
+        if (alive[ch]) cd[ch] = cand[ch * 32 + lane];
+    }
+    constexpr int U = NCH <= 2 ? 8 : 4;
+    bool done = false;
+    for (int eb = 0; eb < cnt && !done; eb += 32) {
+        Lmer<W> mine;
+        if (eb + lane < cnt) mine = T[entries[st + eb + lane] & ID_MASK];
+        const int lim = min(32, cnt - eb);
+        for (int x0 = 0; x0 < lim; x0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int x = x0 + u;
+                const Lmer<W> V = shfl_lmer<W>(mine, x & 31);
+                if (x < lim) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) hit[ch] |= dist<W>(cd[ch], V) <= d;
+                }
+            }
+            scanned += min(U, lim - x0);
+            bool all = true;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) all &= hit[ch] || !alive[ch];
+            if (__all_sync(0xffffffffu, all)) {
+                done = true;
+                break;
+            }
+        }
+    }
+    __syncwarp();
+    int out = 0;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const bool keep = alive[ch] && hit[ch];
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) cand[out + __popc(bal & lanemask_lt())] = cd[ch];
+        out += __popc(bal);
+    }
+    __syncwarp();
+    return out;
+}
+
+// Breadth-first verification of the buffered candidates against the level's
+// rows, smallest row first (verify_candidate checks rows in size order and
+// stops at the first row without a witness); survivors are emitted as keys.
+template <int W, int MT>
+__device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, const uint32_t* entries, int ncand) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane;
+    const int d = P.d;
+    int n = ncand;
+    unsigned long long vcmp = 0;
+    for (int r = 0; r < L.nrows && n > 0; ++r) {
+        const int j = C.S->vorder[r];
+        const int st = L.start[j], cnt = L.cnt[j];
+        int scanned = 0, out = 0;
+        switch ((n + 31) >> 5) {
+            case 1: out = verify_row<W, 1>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+            case 2: out = verify_row<W, 2>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+            case 3: out = verify_row<W, 3>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+            case 4: out = verify_row<W, 4>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+            default: out = verify_row<W, 5>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+        }
+        vcmp += static_cast<unsigned long long>(n) * scanned;
+        n = out;
+    }
+    C.add(W_VCMP, vcmp);
+    // emit the survivors as packed keys
+    for (int base = 0; base < n; base += 32) {
+        const bool alive = base + lane < n;
+        const unsigned em = __ballot_sync(0xffffffffu, alive);
+        unsigned long long pos0 = 0;
+        if (lane == 0) pos0 = atomicAdd(P.key_count, static_cast<unsigned long long>(__popc(em)));
+        pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+        if (alive) {
+            const unsigned long long pos = pos0 + __popc(em & lanemask_lt());
+            if (static_cast<long long>(pos) < P.key_cap) {
+                unsigned long long klo, khi;
+                make_key<W>(C.cand[base + lane], P.l, klo, khi);
+                P.keys[2 * pos] = klo;
+                P.keys[2 * pos + 1] = khi;
+            }
+        }
+        C.add(W_EMIT, __popc(em));
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- enumeration
+// Per-tuple suffix tables (NeighborhoodEnumerator::prepare, :164-226):
+// eq[p] (members holding each symbol), pair suffix distances, Theorem-1
+// triple thresholds (Cd3 = (h_ij + h_ih + h_jh + n4) / 2 of the suffix) and
+// the consensus suffix bound, plus the verification row order.
+template <int W, int MT>
+__device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const LevelMeta& L, Lmer<W>* Tm) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane, l = P.l;
+    WarpFixed& S = *C.S;
+    const int np = P.plan.npair, ntot = P.plan.npair + P.plan.ntri;
+    for (int p = lane; p <= l; p += 32) {
+        uint32_t e = 0;
+        if (p < l) {
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < t) e |= 1u << (8 * code_at<W>(Tm[i], p) + i);
+            S.eq[p] = e;
+        }
+        uint8_t* row = C.thr + p * ntot;
+#pragma unroll
+        for (int j = 1; j < MT; ++j)
+#pragma unroll
+            for (int i = 0; i < j; ++i)
+                if (j < t) row[j * (j - 1) / 2 + i] = static_cast<uint8_t>(suffix_popc<W>(mism<W>(Tm[i], Tm[j]), p));
+#pragma unroll
+        for (int h = 2; h < MT; ++h)
+#pragma unroll
+            for (int j = 1; j < h; ++j)
+#pragma unroll
+                for (int i = 0; i < j; ++i)
+                    if (h < t) {
+                        const Mask<W> mij = mism<W>(Tm[i], Tm[j]);
+                        const Mask<W> mih = mism<W>(Tm[i], Tm[h]);
+                        const Mask<W> mjh = mism<W>(Tm[j], Tm[h]);
+                        Mask<W> n4;
+#pragma unroll
+                        for (int x = 0; x < W; ++x) n4.w[x] = mij.w[x] & mih.w[x] & mjh.w[x];
+                        const int v = (suffix_popc<W>(mij, p) + suffix_popc<W>(mih, p) + suffix_popc<W>(mjh, p) +
+                                       suffix_popc<W>(n4, p)) / 2;
+                        row[np + h * (h - 1) * (h - 2) / 6 + j * (j - 1) / 2 + i] = static_cast<uint8_t>(v);
+                    }
+    }
+    __syncwarp();
+    int carry = 0;
+    const int nchunk = (l + 32) / 32;
+    for (int ch = nchunk - 1; ch >= 0; --ch) {
+        const int p = ch * 32 + lane;
+        int v = 0;
+        if (p < l) {
+            const uint32_t e = S.eq[p];
+            const int best = max(max(__popc(e & 0xFFu), __popc(e & 0xFF00u)),
+                                 max(__popc(e & 0xFF0000u), __popc(e & 0xFF000000u)));
+            v = t - best;
+        }
+        int incl = v;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            const int x = __shfl_down_sync(0xffffffffu, incl, s);
+            if (lane + s < 32) incl += x;
+        }
+        if (p <= l) S.cons[p] = static_cast<uint8_t>(incl + carry);
+        carry += __shfl_sync(0xffffffffu, incl, 0);
+    }
+    if (lane < L.nrows) {
+        const int c = L.cnt[lane];
+        int rank = 0;
+        for (int q = 0; q < L.nrows; ++q) {
+            const int cq = L.cnt[q];
+            rank += (cq < c) || (cq == c && q < lane);
+        }
+        S.vorder[rank] = static_cast<uint8_t>(lane);
+    }
+    __syncwarp();
+}
+
+// Evaluate child (node, symbol c). Returns ok; writes child + leaf flag.
+template <int W, int MT>
+__device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node<W>& nd, int c, int t, uint32_t tmask,
+                                             int prune, Node<W>& ch, bool& leaf) {
+    const SearchParams& P = *C.P;
+    const WarpFixed& S = *C.S;
+    const int p = static_cast<int>(nd.rB >> 24);
+    const uint32_t em = (S.eq[p] >> (8 * c)) & tmask;  // members matching symbol c
+    const uint32_t mm = ~em & tmask;                   // members charged on this edge
+    int r[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const uint32_t word = i < 4 ? nd.rA : nd.rB;
+        r[i] = static_cast<int>((word >> (8 * (i & 3))) & 0xFFu) - 64 - static_cast<int>((mm >> i) & 1u);
+    }
+    ch.c = nd.c;
+    set_code<W>(ch.c, p, c);
+    const int q = p + 1;
+    bool neg = false;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+        if (i < t) neg |= r[i] < 0;
+    leaf = q == P.l;
+    bool ok;
+    if (leaf) {
+        ok = !neg;
+    } else if (prune == 0 || mm == 0) {
+        ok = true;
+    } else {
+        ok = !neg;
+        const uint8_t* row = C.thr + q * (P.plan.npair + P.plan.ntri);
+        if (ok) {
+#pragma unroll
+            for (int j = 1; j < MT; ++j)
+#pragma unroll
+                for (int i = 0; i < j; ++i)
+                    if (j < t) ok &= row[j * (j - 1) / 2 + i] <= r[i] + r[j];
+        }
+        if (ok && prune == 2) {
+#pragma unroll
+            for (int h = 2; h < MT; ++h)
+#pragma unroll
+                for (int j = 1; j < h; ++j)
+#pragma unroll
+                    for (int i = 0; i < j; ++i)
+                        if (h < t)
+                            ok &= row[P.plan.npair + h * (h - 1) * (h - 2) / 6 + j * (j - 1) / 2 + i] <=
+                                  r[i] + r[j] + r[h];
+            int sum = 0;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < t) sum += r[i];
+            if (t >= 2) ok &= S.cons[q] <= sum;
+        }
+    }
+    uint32_t rA = 0, rB = 0;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const uint32_t b = static_cast<uint32_t>(r[i] + 64) & 0xFFu;
+        if (i < 4) rA |= b << (8 * i);
+        else rB |= b << (8 * (i - 4));
+    }
+    ch.rA = rA;
+    ch.rB = rB | (static_cast<uint32_t>(q) << 24);
+    return ok;
+}
+
+// Common d-neighbourhood of the t-tuple on the stack + verification. The
+// DFS starts from the root, or (ndon > 0) from ndon donated nodes already
+// copied to the bottom of the node stack.
+template <int W, int MT>
+__device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane;
+    WarpFixed& S = *C.S;
+    const LevelMeta& L = S.lev[t];
+    const uint32_t* entries = level_entries<W, MT>(C, t);
+    const long long c0 = clock64();
+
+    Lmer<W> Tm[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+        if (i < t) Tm[i] = C.T[S.stack_id[i] & ID_MASK];
+    prepare_tuple<W, MT>(C, t, L, Tm);
+
+    const uint32_t tmask = (1u << t) - 1u;
+    // node stack: circular buffer of NS nodes in shared memory; chunks of
+    // SPILL bottom nodes move to a per-warp global overflow LIFO when it
+    // fills, and come back when it drains (all hot accesses are LDS/STS)
+    constexpr int NS = NodeSmem<W>::N;
+    constexpr int SPILL = NS / 4;
+    Node<W>* ns = C.node_smem;
+    Node<W>* ov = C.node_glob;
+    int bot = 0, nn = 0, nov = 0;
+    if (ndon > 0) {
+        nn = ndon;
+    } else {
+        if (lane == 0) {
+            Node<W> root;
+#pragma unroll
+            for (int i = 0; i < W; ++i) root.c.h[i] = root.c.o[i] = 0;
+            const uint32_t b = static_cast<uint32_t>(P.d + 64);
+            root.rA = b | (b << 8) | (b << 16) | (b << 24);
+            root.rB = b | (b << 8);
+            ns[0] = root;
+        }
+        nn = 1;
+    }
+    __syncwarp();
+    const int prune = P.prune;
+    const int cand_cap = P.plan.cand_cap;
+    unsigned long long nodes = 0, leaves = 0;
+    int ncand = 0, rounds = 0;
+    while (nn > 0 || nov > 0) {
+        if (nn == 0) {  // refill from the overflow
+            nov -= SPILL;
+            if (lane < SPILL) ns[(bot + lane) & (NS - 1)] = ov[nov + lane];
+            nn = SPILL;
+            __syncwarp();
+        }
+        // donate the shallowest nodes when other warps are starving
+        if (P.donate && ((++rounds & 7) == 0) && (nov >= NDON || nn >= NDON + 16) && starving<W, MT>(C)) {
+            TaskHeader h;
+            h.anchor = C.anchor;
+            h.kind = 1;
+            h.k = static_cast<int16_t>(t);
+            h.a0 = NDON;
+            h.a1 = 0;
+#pragma unroll
+            for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
+            h.pad[0] = h.pad[1] = 0;
+            if (nov >= NDON) {
+                const int o0 = nov - NDON;
+                publish<W, MT>(C, h, NDON, [&](int x) { return ov[o0 + x]; });
+                nov -= NDON;
+            } else {
+                const int b0 = bot;
+                publish<W, MT>(C, h, NDON, [&](int x) { return ns[(b0 + x) & (NS - 1)]; });
+                bot = (bot + NDON) & (NS - 1);
+                nn -= NDON;
+            }
+            continue;
+        }
+        bool overflow = false;
+        while (nn > NS - 48) {  // spill bottom chunks: a round may add 48 nodes net
+            if (nov + SPILL > P.node_cap) {
+                if (lane == 0) atomicOr(P.error_flag, 2);
+                overflow = true;
+                break;
+            }
+            if (lane < SPILL) ov[nov + lane] = ns[(bot + lane) & (NS - 1)];
+            nov += SPILL;
+            bot = (bot + SPILL) & (NS - 1);
+            nn -= SPILL;
+            __syncwarp();
+        }
+        if (overflow) break;
+        const int take = min(16, nn);
+        const int base = nn - take;
+        const int slot = lane >> 1;
+        const bool active = slot < take;
+        Node<W> nd;
+        if (active) nd = ns[(bot + base + slot) & (NS - 1)];
+        __syncwarp();
+        nodes += take;
+        Node<W> ch0, ch1;
+        bool leaf0 = false, leaf1 = false, ok0 = false, ok1 = false;
+        if (active) {
+            const int c = (lane & 1) * 2;
+            ok0 = expand_child<W, MT>(C, nd, c, t, tmask, prune, ch0, leaf0);
+            ok1 = expand_child<W, MT>(C, nd, c + 1, t, tmask, prune, ch1, leaf1);
+        }
+        // leaves -> candidate buffer; internal children -> stack
+        const unsigned lb0 = __ballot_sync(0xffffffffu, ok0 && leaf0);
+        const unsigned lb1 = __ballot_sync(0xffffffffu, ok1 && leaf1);
+        const unsigned ib0 = __ballot_sync(0xffffffffu, ok0 && !leaf0);
+        const unsigned ib1 = __ballot_sync(0xffffffffu, ok1 && !leaf1);
+        const unsigned lt = lanemask_lt();
+        if (ok0 && leaf0) C.cand[ncand + __popc(lb0 & lt)] = ch0.c;
+        if (ok1 && leaf1) C.cand[ncand + __popc(lb0) + __popc(lb1 & lt)] = ch1.c;
+        const int nl = __popc(lb0) + __popc(lb1);
+        if (ok0 && !leaf0) ns[(bot + base + __popc(ib0 & lt)) & (NS - 1)] = ch0;
+        if (ok1 && !leaf1) ns[(bot + base + __popc(ib0) + __popc(ib1 & lt)) & (NS - 1)] = ch1;
+        ncand += nl;
+        leaves += nl;
+        nn = base + __popc(ib0) + __popc(ib1);
+        __syncwarp();
+        if (ncand > cand_cap - 64) {
+            verify_all<W, MT>(C, L, entries, ncand);
+            ncand = 0;
+        }
+    }
+    if (ncand > 0) verify_all<W, MT>(C, L, entries, ncand);
+    C.add(W_TUPLES, ndon > 0 ? 0 : 1);
+    C.add(W_LEAVES, leaves);
+    C.add(W_NODES, nodes);
+    C.add(W_CLKP, static_cast<unsigned long long>(clock64() - c0));
+}
+
+// ---------------------------------------------------------------- DFS driver
+// Depth-first over levels kmin..t-1 (recurse, src/solver.cpp:406-419), the
+// branch range of level kmin given by the task.
+template <int W, int MT>
+__device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
+    const SearchParams& P = *C.P;
+    WarpFixed& S = *C.S;
+    const int t = P.t;
+    if (C.lane == 0) {
+        S.iter[kmin] = it0;
+        S.iter_end[kmin] = it1;
+    }
+    __syncwarp();
+    int k = kmin;
+    while (k >= kmin) {
+        const LevelMeta& L = S.lev[k];
+        const int it = S.iter[k];
+        if (it >= S.iter_end[k]) {
+            --k;
+            continue;
+        }
+        const uint32_t uu = level_entries<W, MT>(C, k)[L.start[L.branch] + it];
+        __syncwarp();
+        if (C.lane == 0) {
+            S.iter[k] = it + 1;
+            S.stack_id[k] = uu;
+        }
+        __syncwarp();
+        maybe_donate_dfs<W, MT>(C, kmin, k);
+        if (!filter_push<W, MT>(C, k)) continue;
+        if (k + 1 == t) {
+            enumerate_verify<W, MT>(C, t, 0);
+        } else {
+            ++k;
+            if (C.lane == 0) {
+                S.iter[k] = 0;
+                S.iter_end[k] = S.lev[k].cnt[S.lev[k].branch];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Load the anchor's level-1 row table and set stack[0].
+template <int W, int MT>
+__device__ void begin_anchor(WarpCtx<W, MT>& C, int ai) {
+    const SearchParams& P = *C.P;
+    WarpFixed& S = *C.S;
+    C.anchor = ai;
+    C.l1 = P.l1_entries + static_cast<size_t>(ai) * P.K;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(P.l1_meta + ai);
+    uint32_t* dstm = reinterpret_cast<uint32_t*>(&S.lev[1]);
+    for (int x = C.lane; x < static_cast<int>(sizeof(LevelMeta) / 4); x += 32) dstm[x] = src[x];
+    if (C.lane == 0) S.stack_id[0] = static_cast<uint32_t>(P.anchor_off[ai]);
+    __syncwarp();
+}
+
+}  // namespace
+
+template <int W, int MT>
+__global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    Lmer<W>* T = reinterpret_cast<Lmer<W>*>(smem);
+    const Lmer<W>* gT = static_cast<const Lmer<W>*>(P.table);
+    for (int i = threadIdx.x; i < P.K; i += blockDim.x) T[i] = gT[i];
+    const size_t table_bytes = (static_cast<size_t>(P.K) * sizeof(Lmer<W>) + 15) / 16 * 16;
+    uint8_t* wbase = smem + table_bytes + static_cast<size_t>(P.plan.bytes) * warp;
+    __syncthreads();
+
+    WarpCtx<W, MT> C;
+    C.P = &P;
+    C.T = T;
+    C.S = reinterpret_cast<WarpFixed*>(wbase);
+    C.thr = wbase + P.plan.off_thr;
+    C.cand = reinterpret_cast<Lmer<W>*>(wbase + P.plan.off_cand);
+    C.node_smem = reinterpret_cast<Node<W>*>(wbase + P.plan.off_nodes);
+    const size_t gw = static_cast<size_t>(blockIdx.x) * nwarps + warp;
+    uint32_t* scratch = P.scratch + gw * P.scratch_words;
+    C.lvl_glob = scratch;
+    C.node_glob = reinterpret_cast<Node<W>*>(scratch + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap);
+    C.lane = lane;
+    C.pushes_since_check = 0;
+    if (lane < 16) C.S->ctr[lane] = 0;
+    __syncwarp();
+    WarpFixed& S = *C.S;
+    const int t = P.t;
+    const unsigned long long nstatic = static_cast<unsigned long long>(P.task_base[P.nanchors]);
+    QueueState* qs = P.qs;
+    const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
+    bool waiting = false;
+    long long wait_t0 = 0;
+
+    for (;;) {
+        // ---- claim a task (lane 0), protocol in DESIGN.md §4
+        int kind = -1;  // -1 none, 0 static, 1 dynamic, 2 terminate
+        unsigned long long idx = 0;
+        if (lane == 0) {
+            const bool have_static = ld_volatile(&qs->static_next) < nstatic;
+            const unsigned long long h0 = ld_volatile(&qs->head);
+            const bool have_dyn = ld_volatile(&P.qstate[h0 % qcap]) == 2u * static_cast<unsigned int>(h0 / qcap) + 1u;
+            if (have_static || have_dyn) {
+                // announce before claiming so that no waiter can observe
+                // busy == 0 while a claimed task is still unannounced
+                atomicAdd(&qs->busy, 1u);
+                if (have_static) {
+                    idx = atomicAdd(&qs->static_next, 1ull);
+                    if (idx < nstatic) kind = 0;
+                }
+                if (kind < 0) {
+                    const unsigned long long h = ld_volatile(&qs->head);
+                    if (ld_volatile(&P.qstate[h % qcap]) == 2u * static_cast<unsigned int>(h / qcap) + 1u &&
+                        atomicCAS(&qs->head, h, h + 1) == h) {
+                        kind = 1;
+                        idx = h;
+                        __threadfence();
+                    }
+                }
+                if (kind < 0) atomicSub(&qs->busy, 1u);
+            }
+            if (kind < 0) {
+                if (!waiting) {
+                    atomicAdd(&qs->waiting, 1u);
+                    waiting = true;
+                    wait_t0 = clock64();
+                }
+                __threadfence();
+                if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
+                    ld_volatile(&qs->static_next) >= nstatic) {
+                    kind = 2;
+                } else if (clock64() - wait_t0 > (1ll << 35)) {
+                    atomicOr(P.error_flag, 8);  // watchdog: ~17 s without work
+                    kind = 2;
+                } else {
+                    __nanosleep(500);
+                }
+            } else if (waiting) {
+                atomicSub(&qs->waiting, 1u);
+                waiting = false;
+            }
+        }
+        kind = __shfl_sync(0xffffffffu, kind, 0);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (kind == 2) {
+            if (lane == 0 && waiting) atomicSub(&qs->waiting, 1u);
+            break;
+        }
+        if (kind < 0) continue;
+        const long long task_t0 = clock64();
+        C.add(W_TASKS, 1);
+        if (kind == 0) {
+            // anchor: last a with task_base[a] <= idx
+            int lo = 0, hi = P.nanchors - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (static_cast<unsigned long long>(P.task_base[mid]) <= idx) lo = mid;
+                else hi = mid - 1;
+            }
+            begin_anchor<W, MT>(C, lo);
+            const int j = static_cast<int>(idx - static_cast<unsigned long long>(P.task_base[lo]));
+            if (t == 1) enumerate_verify<W, MT>(C, 1, 0);
+            else dfs<W, MT>(C, 1, j, j + 1);
+        } else {
+            const uint8_t* slot = P.qslots + (idx % static_cast<unsigned long long>(P.qcap)) * P.qslot_bytes;
+            const uint32_t* hs = reinterpret_cast<const uint32_t*>(slot);
+            uint32_t* hd = reinterpret_cast<uint32_t*>(&S.task);
+            for (int x = lane; x < static_cast<int>(sizeof(TaskHeader) / 4); x += 32) hd[x] = __ldcg(hs + x);
+            __syncwarp();
+            // copy donated nodes out of the slot right away (the ring reuses it)
+            const int ndon = S.task.kind == 1 ? S.task.a0 : 0;
+            {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(slot + sizeof(TaskHeader));
+                constexpr int NW = sizeof(Node<W>) / 4;
+                for (int x = lane; x < ndon; x += 32) {
+                    Node<W> nd;
+                    uint32_t* w = reinterpret_cast<uint32_t*>(&nd);
+#pragma unroll
+                    for (int q = 0; q < NW; ++q) w[q] = __ldcg(src + x * NW + q);
+                    C.node_smem[x] = nd;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(&P.qstate[idx % qcap], 2u * static_cast<unsigned int>(idx / qcap) + 2u);
+            }
+            const int tk = S.task.k;
+            begin_anchor<W, MT>(C, S.task.anchor);
+            if (lane < MAXT && lane >= 1 && lane < tk) S.stack_id[lane] = S.task.stack[lane];
+            __syncwarp();
+            // replay the prefix pushes to rebuild levels 2..tk
+            bool ok = true;
+            for (int i = 1; i < tk && ok; ++i) {
+                ok = filter_push<W, MT>(C, i);
+                C.add(W_REPLAYS, 1);
+                C.add(W_PUSH, ~0ull);  // replays are not new tree nodes
+                if (ok) C.add(W_VIABLE, ~0ull);
+            }
+            if (!ok) {
+                if (lane == 0) atomicOr(P.error_flag, 4);
+            } else if (S.task.kind == 0) {
+                dfs<W, MT>(C, tk, S.task.a0, S.task.a1);
+            } else {
+                enumerate_verify<W, MT>(C, tk, ndon);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicSub(&qs->busy, 1u);
+            const long long dt = clock64() - task_t0;
+            atomicAdd(P.counters + C_HIST0 + min(39, 63 - __clzll(dt > 0 ? dt : 1)), 1ull);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const int map[W_N] = {C_PUSHES, C_VIABLE, C_SLOTS, C_TUPLES, C_LEAVES, C_EMITTED, C_VCMP, C_NODES,
+                              C_PAIR_REJ, C_TRI_REJ, C_TASKS, C_DONATED, C_REPLAYS, C_CLK_FILTER, C_CLK_PATTERN};
+#pragma unroll
+        for (int i = 0; i < W_N; ++i) atomicAdd(P.counters + map[i], S.ctr[i]);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+
+template <int W>
+WarpPlan make_plan_t(int l, int t) {
+    WarpPlan p{};
+    const int tt = t < 1 ? 1 : t;
+    p.npair = tt * (tt - 1) / 2;
+    p.ntri = tt * (tt - 1) * (tt - 2) / 6;
+    int off = (static_cast<int>(sizeof(WarpFixed)) + 15) / 16 * 16;
+    p.off_thr = off;
+    off += ((l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
+    p.cand_cap = 32 * MAXCH;
+    p.off_cand = off;
+    off += p.cand_cap * static_cast<int>(sizeof(Lmer<W>));
+    off = (off + 15) / 16 * 16;
+    p.node_smem = NodeSmem<W>::N;
+    p.off_nodes = off;
+    off += p.node_smem * static_cast<int>(sizeof(Node<W>));
+    p.bytes = (off + 15) / 16 * 16;
+    return p;
+}
+
+WarpPlan make_plan(int W, int l, int t) { return W == 1 ? make_plan_t<1>(l, t) : make_plan_t<2>(l, t); }
+
+size_t node_bytes(int W) { return W == 1 ? sizeof(Node<1>) : sizeof(Node<2>); }
+
+size_t search_smem(int W, int K, int warps, const WarpPlan& plan) {
+    return (static_cast<size_t>(K) * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
+}
+
+size_t task_slot_bytes(int W) { return (sizeof(TaskHeader) + NDON * node_bytes(W) + 127) / 128 * 128; }
+
+template <int W, int MT>
+cudaError_t set_smem_t(size_t bytes) {
+    return cudaFuncSetAttribute(search_kernel<W, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes));
+}
+
+// The kernel is specialised on the switch depth (tuple size) so that every
+// per-member loop is unrolled over registers; t = 1 runs the MT = 2 build.
+cudaError_t set_search_smem(int W, int t, size_t bytes) {
+    const int mt = t < 2 ? 2 : t;
+#define PMS8G_CASE(WW, M) \
+    if (W == WW && mt == M) return set_smem_t<WW, M>(bytes);
+    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
+    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6)
+#undef PMS8G_CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s) {
+    const int mt = P.t < 2 ? 2 : P.t;
+#define PMS8G_CASE(WW, M)                                                 \
+    if (W == WW && mt == M) {                                             \
+        search_kernel<WW, M><<<blocks, warps * 32, smem, s>>>(P);         \
+        return cudaGetLastError();                                        \
+    }
+    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
+    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6)
+#undef PMS8G_CASE
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace pms8g

@@ -1,0 +1,33 @@
+"""Run one config on the GPU and print timing + device counters (diagnostics).
+usage: python scripts/profile_run.py L D [t] [reps] [anchors-stride]"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1307_0571_b200 as P  # noqa: E402
+
+l, d = int(sys.argv[1]), int(sys.argv[2])
+t = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+stride = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+inst = P.generate_planted_instance(P.PlantedInstanceSpec(l=l, d=d, seed=1, mutation=P.MutationMode.exactly_d))
+anchors = list(range(0, 600 - l + 1, stride)) if stride > 1 else None
+ctx = P.Context(20, 600, l, d, P.Alphabet.dna(), P.SolverConfig(threshold_override=t or None),
+                P.ParallelOptions(anchors=anchors))
+ctx.load_codes(inst.codes.ctypes.data, False)
+for r in range(reps):
+    t0 = time.perf_counter()
+    ctx.run()
+    dt = time.perf_counter() - t0
+rep = P.RunReport()
+motifs = ctx.result(rep)
+c = ctx.counters()
+names = ["pushes", "viable", "slots", "tuples", "leaves", "emitted", "vcmp", "nodes", "clk_filter", "clk_pattern",
+         "pair_rej", "tri_rej", "tasks", "donated", "replays"]
+print(f"({l},{d}) t={rep.threshold} anchors={rep.subproblems} wall={dt*1e3:.2f}ms search={ctx.kernel_ms()[0]:.2f}ms "
+      f"motifs={motifs}")
+print("  " + " ".join(f"{n}={v}" for n, v in zip(names, c)))
+hist = c[15:55]
+print("  task cycles histogram (log2 bucket: count): " +
+      " ".join(f"{i}:{v}" for i, v in enumerate(hist) if v))

@@ -185,3 +185,17 @@ def test_cli_solve_matches_reference_stdout(tmp_path):
     g.write_text("AAAAAAAA\nCCCCCCCC\n")
     r = subprocess.run([exe, "solve", str(g), "-l", "8", "-d", "0"], capture_output=True, text=True)
     assert r.returncode == 1 and r.stdout == ""
+
+
+def test_work_queue_wraparound_keeps_every_node(monkeypatch):
+    # a 16-slot ring forces producers to wrap many times; the search tree must
+    # still be the reference's exactly (no donated node lost or duplicated)
+    g = golden("planted_13_4.json")[0]
+    inst = planted(13, 4, 1)
+    monkeypatch.setenv("PMS8G_QCAP", "16")
+    rep = P.RunReport()
+    got = P.run_parallel(inst.problem, P.SolverConfig(threshold_override=2), P.ParallelOptions(warps_per_block=15),
+                         rep)
+    assert got == g["motifs"]
+    assert rep.counters.neighbors_visited == g["report"]["neighbors_visited"]
+    assert rep.counters.motifs_emitted == g["report"]["motifs_emitted"]
