@@ -12,6 +12,7 @@ it writes are committed and travel to the GPU box.
     python tests/golden/make_golden.py heavy21      # (21,8) anchor sample
     python tests/golden/make_golden.py heavy23      # (23,9) anchor sample
     python tests/golden/make_golden.py heavy50      # (50,21) depth-1 branch sample
+    python tests/golden/make_golden.py heavyplanted # (21,8)/(23,9) planted S1 offsets
 """
 import hashlib
 import json
@@ -170,6 +171,11 @@ def main():
         anchor_sample(21, 8, 1, list(range(0, 580, 37)), "anchors_21_8.json")
     elif what == "heavy23":
         anchor_sample(23, 9, 1, list(range(0, 578, 72)), "anchors_23_9.json")
+    elif what == "heavyplanted":
+        # the S1 offset holding the planted occurrence (190 for seed 1), so the
+        # heavy-config anchor parity includes a non-empty motif set
+        anchor_sample(21, 8, 1, [190, 189, 191], "anchors_21_8_planted.json")
+        anchor_sample(23, 9, 1, [190], "anchors_23_9_planted.json")
     elif what == "heavy50":
         samples = [branch_sample(50, 21, 1, 0, [0, 1, 3], "x")]
         dump("branches_50_21.json", samples)
