@@ -561,6 +561,167 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
     return ok;
 }
 
+
+// ---------------------------------------------------------------- SWAR path (t <= 4)
+// Budgets of up to 4 tuple members live in one word, one byte each (r_i >= 0,
+// unused members pinned at 0). Per tuple and position p, DEC[p][c] holds
+// [s_i[p] != c] in byte i, so a child's budgets are (R | 0x80..) - DEC with no
+// cross-byte borrow and a cleared bit 7 flags an exhausted budget. Per suffix
+// start q, THR[q] packs the pair thresholds [01,12,23,02], [13,03,cons,-] and
+// the Theorem-1 triple thresholds [012,123,013,023]; the pair sums and triple
+// sums come from three shifted adds and are compared bytewise. Same rules as
+// NeighborhoodEnumerator::prune (src/neighborhood.cpp:228-270), branch-free.
+__device__ __forceinline__ bool bytes_ge(uint32_t x, uint32_t y) {
+    return (((x | 0x80808080u) - y) & 0x80808080u) == 0x80808080u;
+}
+
+template <int W, int MT>
+__device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const LevelMeta& L, const Lmer<W>* Tm) {
+    const int lane = C.lane, l = C.P->l;
+    WarpFixed& S = *C.S;
+    uint32_t* dec = reinterpret_cast<uint32_t*>(C.thr);          // [l][4]
+    uint4* thr = reinterpret_cast<uint4*>(C.thr + 16 * ((l + 3) & ~3) );  // [l+1]
+    const int nchunk = (l + 32) / 32;  // positions 0..l
+    int carry = 0, carry_next = 0;
+    for (int ch = nchunk - 1; ch >= 0; --ch) {
+        const int p = ch * 32 + lane;
+        carry = carry_next;
+        if (p < l) {
+            uint32_t dd[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < t) {
+                    const int ci = code_at<W>(Tm[i], p);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dd[c] |= static_cast<uint32_t>(ci != c) << (8 * i);
+                }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dec[4 * p + c] = dd[c];
+        }
+        uint32_t pr[6] = {0u, 0u, 0u, 0u, 0u, 0u};  // 01,12,23,02,13,03
+        uint32_t tr[4] = {0u, 0u, 0u, 0u};          // 012,123,013,023
+        Mask<W> m[4][4];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = i + 1; j < MT; ++j) m[i][j] = mism<W>(Tm[i], Tm[j]);
+        auto ps = [&](int i, int j) -> uint32_t {
+            return (i < t && j < t) ? static_cast<uint32_t>(suffix_popc<W>(m[i][j], p)) : 0u;
+        };
+        auto ts = [&](int i, int j, int h) -> uint32_t {
+            if (!(i < t && j < t && h < t)) return 0u;
+            Mask<W> n4;
+#pragma unroll
+            for (int x = 0; x < W; ++x) n4.w[x] = m[i][j].w[x] & m[i][h].w[x] & m[j][h].w[x];
+            return static_cast<uint32_t>((suffix_popc<W>(m[i][j], p) + suffix_popc<W>(m[i][h], p) +
+                                          suffix_popc<W>(m[j][h], p) + suffix_popc<W>(n4, p)) / 2);
+        };
+        if (MT >= 2) pr[0] = ps(0, 1);
+        if (MT >= 3) {
+            pr[1] = ps(1, 2);
+            pr[3] = ps(0, 2);
+            tr[0] = ts(0, 1, 2);
+        }
+        if (MT >= 4) {
+            pr[2] = ps(2, 3);
+            pr[4] = ps(1, 3);
+            pr[5] = ps(0, 3);
+            tr[1] = ts(1, 2, 3);
+            tr[2] = ts(0, 1, 3);
+            tr[3] = ts(0, 2, 3);
+        }
+        // consensus suffix bound: column cost t - max frequency, summed over
+        // the suffix by a reverse scan across lanes (two chunks for l > 31)
+        uint32_t cons = 0;
+        {
+            int v = 0;
+            if (p < l) {
+                int f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    if (i < t) {
+                        const int ci = code_at<W>(Tm[i], p);
+                        f0 += ci == 0;
+                        f1 += ci == 1;
+                        f2 += ci == 2;
+                        f3 += ci == 3;
+                    }
+                v = t - max(max(f0, f1), max(f2, f3));
+            }
+            int incl = v;
+#pragma unroll
+            for (int sh = 1; sh < 32; sh <<= 1) {
+                const int x = __shfl_down_sync(0xffffffffu, incl, sh);
+                if (lane + sh < 32) incl += x;
+            }
+            // carry from the later chunk (positions p + 32 ...) is added below
+            cons = static_cast<uint32_t>(incl) + static_cast<uint32_t>(carry);
+            carry_next = __shfl_sync(0xffffffffu, incl, 0) + carry;
+        }
+        // budgets are <= d <= 31 here, so every sum is <= 124: clamping the
+        // thresholds at 127 keeps the bytewise compares borrow-free
+#pragma unroll
+        for (int x = 0; x < 6; ++x) pr[x] = min(pr[x], 127u);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) tr[x] = min(tr[x], 127u);
+        cons = min(cons, 127u);
+        if (p <= l) {
+            uint4 w;
+            w.x = pr[0] | (pr[1] << 8) | (pr[2] << 16) | (pr[3] << 24);
+            w.y = pr[4] | (pr[5] << 8) | (cons << 16);
+            w.z = tr[0] | (tr[1] << 8) | (tr[2] << 16) | (tr[3] << 24);
+            w.w = 0;
+            thr[p] = w;
+        }
+    }
+    if (lane < L.nrows) {
+        const int c = L.cnt[lane];
+        int rank = 0;
+        for (int q = 0; q < L.nrows; ++q) {
+            const int cq = L.cnt[q];
+            rank += (cq < c) || (cq == c && q < lane);
+        }
+        S.vorder[rank] = static_cast<uint8_t>(lane);
+    }
+    __syncwarp();
+}
+
+template <int W, int MT>
+__device__ __forceinline__ bool expand_child_swar(const WarpCtx<W, MT>& C, const Node<W>& nd, int c, int prune,
+                                                  Node<W>& ch, bool& leaf) {
+    const int l = C.P->l;
+    const uint32_t* dec = reinterpret_cast<const uint32_t*>(C.thr);
+    const uint4* thr = reinterpret_cast<const uint4*>(C.thr + 16 * ((l + 3) & ~3));
+    const int p = static_cast<int>(nd.rB >> 24);
+    const uint32_t D = dec[4 * p + c];
+    uint32_t R = (nd.rA | 0x80808080u) - D;
+    bool ok = (R & 0x80808080u) == 0x80808080u;
+    R &= 0x7F7F7F7Fu;
+    const int q = p + 1;
+    leaf = q == l;
+    if (!leaf && prune != 0 && D != 0u) {
+        const uint4 T = thr[q];
+        const uint32_t r3 = R >> 24;
+        const uint32_t A1 = R + (R >> 8);    // [01, 12, 23, 3]
+        const uint32_t A2 = R + (R >> 16);   // [02, 13, 2, 3]
+        const uint32_t A3 = R + r3;          // [03, 1, 2, 3]
+        const uint32_t P1 = (A1 & 0x00FFFFFFu) | (A2 << 24);                      // [01,12,23,02]
+        const uint32_t S3 = A1 + (R >> 16);                                       // [012, 123, ..]
+        const uint32_t cons = (S3 + r3) & 0xFFu;                                  // r0+r1+r2+r3
+        const uint32_t P2 = ((A2 >> 8) & 0xFFu) | ((A3 & 0xFFu) << 8) | (cons << 16);  // [13,03,cons,0]
+        const uint32_t B1 = (A1 + r3) & 0xFFu;                                    // 013
+        const uint32_t B2 = (A2 + r3) & 0xFFu;                                    // 023
+        const uint32_t T3 = (S3 & 0xFFFFu) | (B1 << 16) | (B2 << 24);             // [012,123,013,023]
+        ok = ok && bytes_ge(P1, T.x) && bytes_ge(P2, prune == 2 ? T.y : (T.y & 0xFFFFu)) &&
+             (prune != 2 || bytes_ge(T3, T.z));
+    }
+    ch.c = nd.c;
+    set_code<W>(ch.c, p, c);
+    ch.rA = R;
+    ch.rB = static_cast<uint32_t>(q) << 24;
+    return ok;
+}
+
 // Common d-neighbourhood of the t-tuple on the stack + verification. The
 // DFS starts from the root, or (ndon > 0) from ndon donated nodes already
 // copied to the bottom of the node stack.
@@ -577,7 +738,9 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
 #pragma unroll
     for (int i = 0; i < MT; ++i)
         if (i < t) Tm[i] = C.T[S.stack_id[i] & ID_MASK];
-    prepare_tuple<W, MT>(C, t, L, Tm);
+    const bool swar = MT <= 4 && P.d <= 31;
+    if (swar) prepare_tuple_swar<W, MT>(C, t, L, Tm);
+    else prepare_tuple<W, MT>(C, t, L, Tm);
 
     const uint32_t tmask = (1u << t) - 1u;
     // node stack: circular buffer of NS nodes in shared memory; chunks of
@@ -595,9 +758,16 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
             Node<W> root;
 #pragma unroll
             for (int i = 0; i < W; ++i) root.c.h[i] = root.c.o[i] = 0;
-            const uint32_t b = static_cast<uint32_t>(P.d + 64);
-            root.rA = b | (b << 8) | (b << 16) | (b << 24);
-            root.rB = b | (b << 8);
+            if (swar) {
+                uint32_t b = 0;
+                for (int i = 0; i < t; ++i) b |= static_cast<uint32_t>(P.d) << (8 * i);
+                root.rA = b;
+                root.rB = 0;
+            } else {
+                const uint32_t b = static_cast<uint32_t>(P.d + 64);
+                root.rA = b | (b << 8) | (b << 16) | (b << 24);
+                root.rB = b | (b << 8);
+            }
             ns[0] = root;
         }
         nn = 1;
@@ -663,8 +833,13 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
         bool leaf0 = false, leaf1 = false, ok0 = false, ok1 = false;
         if (active) {
             const int c = (lane & 1) * 2;
-            ok0 = expand_child<W, MT>(C, nd, c, t, tmask, prune, ch0, leaf0);
-            ok1 = expand_child<W, MT>(C, nd, c + 1, t, tmask, prune, ch1, leaf1);
+            if (swar) {
+                ok0 = expand_child_swar<W, MT>(C, nd, c, prune, ch0, leaf0);
+                ok1 = expand_child_swar<W, MT>(C, nd, c + 1, prune, ch1, leaf1);
+            } else {
+                ok0 = expand_child<W, MT>(C, nd, c, t, tmask, prune, ch0, leaf0);
+                ok1 = expand_child<W, MT>(C, nd, c + 1, t, tmask, prune, ch1, leaf1);
+            }
         }
         // leaves -> candidate buffer; internal children -> stack
         const unsigned lb0 = __ballot_sync(0xffffffffu, ok0 && leaf0);
@@ -927,7 +1102,9 @@ WarpPlan make_plan_t(int l, int t) {
     p.ntri = tt * (tt - 1) * (tt - 2) / 6;
     int off = (static_cast<int>(sizeof(WarpFixed)) + 15) / 16 * 16;
     p.off_thr = off;
-    off += ((l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
+    const int generic_thr = ((l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
+    const int swar_thr = 16 * ((l + 3) & ~3) + 16 * (l + 1);
+    off += generic_thr > swar_thr ? generic_thr : swar_thr;
     p.cand_cap = 32 * MAXCH;
     p.off_cand = off;
     off += p.cand_cap * static_cast<int>(sizeof(Lmer<W>));
