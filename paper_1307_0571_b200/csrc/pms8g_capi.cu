@@ -369,7 +369,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
 
     const int na = static_cast<int>(c->anchors.size());
-    c->level_cap = c->K;
+    c->level_cap = (c->K + 31) / 32 * 32;  // keeps the per-warp node overflow 16-byte aligned
     c->node_cap = 64 * (l + 4);
     const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
     const size_t node_words = static_cast<size_t>(c->node_cap) * node_bytes(c->W) / 4;

@@ -722,6 +722,155 @@ __device__ __forceinline__ bool expand_child_swar(const WarpCtx<W, MT>& C, const
     return ok;
 }
 
+
+// SWAR check of a child's budget bytes R against the suffix thresholds T of
+// its position (pairs, consensus, Theorem-1 triples), specialised on MT.
+template <int MT>
+__device__ __forceinline__ bool swar_feasible(uint32_t R, const uint4& T, int prune) {
+    if (MT == 2) {
+        const uint32_t s01 = (R + (R >> 8)) & 0xFFu;
+        return s01 >= (T.x & 0xFFu);
+    }
+    const uint32_t r3 = R >> 24;
+    const uint32_t A1 = R + (R >> 8);   // [01, 12, 23, 3]
+    const uint32_t A2 = R + (R >> 16);  // [02, 13, 2, 3]
+    const uint32_t P1 = (A1 & 0x00FFFFFFu) | (A2 << 24);
+    bool ok = bytes_ge(P1, T.x);
+    if (prune == 1) {
+        if (MT == 4) ok = ok && bytes_ge(((A2 >> 8) & 0xFFu) | (((R + r3) & 0xFFu) << 8), T.y & 0xFFFFu);
+        return ok;
+    }
+    const uint32_t S3 = A1 + (R >> 16);  // [012, 123, ...]
+    if (MT == 3) {
+        // pairs 01,12,02 + triple 012 (= the consensus bound for 3 members)
+        return ok && ((S3 & 0xFFu) >= (T.z & 0xFFu));
+    }
+    const uint32_t cons = (S3 + r3) & 0xFFu;
+    const uint32_t P2 = ((A2 >> 8) & 0xFFu) | (((R + r3) & 0xFFu) << 8) | (cons << 16);
+    const uint32_t T3 = (S3 & 0xFFFFu) | (((A1 + r3) & 0xFFu) << 16) | (((A2 + r3) & 0xFFu) << 24);
+    return ok && bytes_ge(P2, T.y) && bytes_ge(T3, T.z);
+}
+
+// Enumeration loop for l <= 32 and t <= 4: nodes are uint4 {h, o, budgets,
+// p<<24}; a round pops 16 nodes, each lane evaluates two sibling children
+// (symbols 2(lane&1) and 2(lane&1)+1) from one LDS.128 node, one LDS.64 of
+// budget decrements and one LDS.128 of suffix thresholds.
+template <int MT>
+__device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const LevelMeta& L, const uint32_t* entries,
+                                            int bot, int nn, int nov, unsigned long long& nodes_out,
+                                            unsigned long long& leaves_out) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane, l = P.l;
+    WarpFixed& S = *C.S;
+    constexpr int NS = NodeSmem<1>::N;
+    constexpr int SPILL = NS / 4;
+    uint4* ns = reinterpret_cast<uint4*>(C.node_smem);
+    uint4* ov = reinterpret_cast<uint4*>(C.node_glob);
+    uint2* cand = reinterpret_cast<uint2*>(C.cand);
+    const uint2* dec2 = reinterpret_cast<const uint2*>(C.thr);
+    const uint4* thr = reinterpret_cast<const uint4*>(C.thr + 16 * ((l + 3) & ~3));
+    const int prune = P.prune;
+    const int cand_cap = P.plan.cand_cap;
+    const uint32_t odd = lane & 1;
+    unsigned long long rounds = 0, leaves = 0, nodes = 0;
+    int ncand = 0;
+    while (nn > 0 || nov > 0) {
+        if (nn == 0) {
+            nov -= SPILL;
+            if (lane < SPILL) ns[(bot + lane) & (NS - 1)] = ov[nov + lane];
+            nn = SPILL;
+            __syncwarp();
+        }
+        if (P.donate && (++rounds & 15) == 0 && (nov >= NDON || nn >= NDON + 16) && starving<1, MT>(C)) {
+            TaskHeader h;
+            h.anchor = C.anchor;
+            h.kind = 1;
+            h.k = static_cast<int16_t>(t);
+            h.a0 = NDON;
+            h.a1 = 0;
+#pragma unroll
+            for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
+            h.pad[0] = h.pad[1] = 0;
+            if (nov >= NDON) {
+                const int o0 = nov - NDON;
+                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_glob[o0 + x]; });
+                nov -= NDON;
+            } else {
+                const int b0 = bot;
+                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem[(b0 + x) & (NS - 1)]; });
+                bot = (bot + NDON) & (NS - 1);
+                nn -= NDON;
+            }
+            continue;
+        }
+        bool overflow = false;
+        while (nn > NS - 48) {
+            if (nov + SPILL > P.node_cap) {
+                if (lane == 0) atomicOr(P.error_flag, 2);
+                overflow = true;
+                break;
+            }
+            if (lane < SPILL) ov[nov + lane] = ns[(bot + lane) & (NS - 1)];
+            nov += SPILL;
+            bot = (bot + SPILL) & (NS - 1);
+            nn -= SPILL;
+            __syncwarp();
+        }
+        if (overflow) break;
+        const int take = min(16, nn);
+        const int base = nn - take;
+        const bool active = (lane >> 1) < take;
+        uint4 nd = make_uint4(0u, 0u, 0u, 0u);
+        if (active) nd = ns[(bot + base + (lane >> 1)) & (NS - 1)];
+        nodes += take;
+        const int p = static_cast<int>(nd.w >> 24);
+        const uint2 D = dec2[2 * p + odd];
+        const uint4 T = thr[p + 1];
+        uint32_t R0 = (nd.z | 0x80808080u) - D.x;
+        uint32_t R1 = (nd.z | 0x80808080u) - D.y;
+        bool ok0 = active && (R0 & 0x80808080u) == 0x80808080u;
+        bool ok1 = active && (R1 & 0x80808080u) == 0x80808080u;
+        R0 &= 0x7F7F7F7Fu;
+        R1 &= 0x7F7F7F7Fu;
+        const bool leaf = p + 1 == l;
+        if (!leaf && prune != 0) {
+            ok0 = ok0 && (D.x == 0u || swar_feasible<MT>(R0, T, prune));
+            ok1 = ok1 && (D.y == 0u || swar_feasible<MT>(R1, T, prune));
+        }
+        const uint32_t bit = 1u << p;
+        const uint32_t h = nd.x | (odd ? bit : 0u);
+        const uint32_t o1 = nd.y | bit;
+        const uint32_t q24 = static_cast<uint32_t>(p + 1) << 24;
+        __syncwarp();
+        const unsigned lt = lanemask_lt();
+        const unsigned lb0 = __ballot_sync(0xffffffffu, ok0 && leaf);
+        const unsigned lb1 = __ballot_sync(0xffffffffu, ok1 && leaf);
+        const unsigned ib0 = __ballot_sync(0xffffffffu, ok0 && !leaf);
+        const unsigned ib1 = __ballot_sync(0xffffffffu, ok1 && !leaf);
+        const int n0 = __popc(ib0);
+        if (ok0) {
+            if (leaf) cand[ncand + __popc(lb0 & lt)] = make_uint2(h, nd.y);
+            else ns[(bot + base + __popc(ib0 & lt)) & (NS - 1)] = make_uint4(h, nd.y, R0, q24);
+        }
+        if (ok1) {
+            if (leaf) cand[ncand + __popc(lb0) + __popc(lb1 & lt)] = make_uint2(h, o1);
+            else ns[(bot + base + n0 + __popc(ib1 & lt)) & (NS - 1)] = make_uint4(h, o1, R1, q24);
+        }
+        const int nl = __popc(lb0) + __popc(lb1);
+        ncand += nl;
+        leaves += nl;
+        nn = base + n0 + __popc(ib1);
+        __syncwarp();
+        if (ncand > cand_cap - 64) {
+            verify_all<1, MT>(C, L, entries, ncand);
+            ncand = 0;
+        }
+    }
+    if (ncand > 0) verify_all<1, MT>(C, L, entries, ncand);
+    nodes_out += nodes;
+    leaves_out += leaves;
+}
+
 // Common d-neighbourhood of the t-tuple on the stack + verification. The
 // DFS starts from the root, or (ndon > 0) from ndon donated nodes already
 // copied to the bottom of the node stack.
@@ -777,6 +926,12 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
     const int cand_cap = P.plan.cand_cap;
     unsigned long long nodes = 0, leaves = 0;
     int ncand = 0, rounds = 0;
+    if constexpr (W == 1) {
+        if (swar) {
+            enum_loop_fast<MT>(C, t, L, entries, bot, nn, nov, nodes, leaves);
+            goto done;
+        }
+    }
     while (nn > 0 || nov > 0) {
         if (nn == 0) {  // refill from the overflow
             nov -= SPILL;
@@ -862,6 +1017,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
         }
     }
     if (ncand > 0) verify_all<W, MT>(C, L, entries, ncand);
+done:
     C.add(W_TUPLES, ndon > 0 ? 0 : 1);
     C.add(W_LEAVES, leaves);
     C.add(W_NODES, nodes);
@@ -961,6 +1117,7 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
     bool waiting = false;
     long long wait_t0 = 0;
+    unsigned int backoff = 128;
 
     for (;;) {
         // ---- claim a task (lane 0), protocol in DESIGN.md §4
@@ -994,8 +1151,8 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
                     atomicAdd(&qs->waiting, 1u);
                     waiting = true;
                     wait_t0 = clock64();
+                    backoff = 128;
                 }
-                __threadfence();
                 if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
                     ld_volatile(&qs->static_next) >= nstatic) {
                     kind = 2;
@@ -1003,7 +1160,10 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
                     atomicOr(P.error_flag, 8);  // watchdog: ~17 s without work
                     kind = 2;
                 } else {
-                    __nanosleep(500);
+                    // idle warps back off so their polling does not steal
+                    // issue slots and L2 bandwidth from the busy ones
+                    __nanosleep(backoff);
+                    backoff = min(backoff * 2, 8192u);
                 }
             } else if (waiting) {
                 atomicSub(&qs->waiting, 1u);
