@@ -35,6 +35,8 @@ struct Node {
     uint32_t rB;  // budgets of members 4..5 (bytes 0,1); prefix length p in byte 3
 };
 
+extern __shared__ __align__(16) uint8_t dyn_smem[];
+
 template <int W>
 struct NodeSmem {
     static constexpr int N = W == 1 ? 128 : 64;  // power of two
@@ -61,19 +63,22 @@ constexpr int MAXCH = 5;  // candidate chunks of 32 held in registers by verify
 template <int W, int MT>
 struct WarpCtx {
     const SearchParams* P;
-    const Lmer<W>* T;  // l-mer table in shared memory
-    WarpFixed* S;
-    uint8_t* thr;      // per-tuple suffix thresholds
-    Lmer<W>* cand;     // candidate buffer
-    Node<W>* node_smem;
+    uint32_t off_S, off_thr, off_cand, off_nodes;  // byte offsets into the dynamic shared memory
     Node<W>* node_glob;
     uint32_t* lvl_glob;
     const uint32_t* l1;  // level-1 entries of the current anchor
     int anchor;          // anchor index of the current task
     int lane;
     int pushes_since_check;
+    // shared-memory views derived from the extern __shared__ symbol, so every
+    // access compiles to LDS/STS rather than generic LD/ST
+    __device__ __forceinline__ const Lmer<W>* T() const { return reinterpret_cast<const Lmer<W>*>(dyn_smem); }
+    __device__ __forceinline__ WarpFixed* S() const { return reinterpret_cast<WarpFixed*>(dyn_smem + off_S); }
+    __device__ __forceinline__ uint8_t* thr() const { return dyn_smem + off_thr; }
+    __device__ __forceinline__ Lmer<W>* cand() const { return reinterpret_cast<Lmer<W>*>(dyn_smem + off_cand); }
+    __device__ __forceinline__ Node<W>* node_smem() const { return reinterpret_cast<Node<W>*>(dyn_smem + off_nodes); }
     __device__ __forceinline__ void add(int i, unsigned long long v) {
-        if (lane == 0) S->ctr[i] += v;
+        if (lane == 0) S()->ctr[i] += v;
     }
 };
 
@@ -96,7 +101,7 @@ template <int W, int MT>
 __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const SearchParams& P = *C.P;
     const int lane = C.lane;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     LevelMeta& Ls = S.lev[k];
     LevelMeta& Ld = S.lev[k + 1];
     const uint32_t* src = level_entries<W, MT>(C, k);
@@ -104,14 +109,14 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const int d = P.d, six_d = 6 * d, two_d = 2 * d;
     const long long f0 = clock64();
 
-    const Lmer<W> U = C.T[S.stack_id[k] & ID_MASK];
+    const Lmer<W> U = C.T()[S.stack_id[k] & ID_MASK];
     Lmer<W> Sm[MT];
     Mask<W> Miu[MT];
     int hs[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         if (i < k) {
-            Sm[i] = C.T[S.stack_id[i] & ID_MASK];
+            Sm[i] = C.T()[S.stack_id[i] & ID_MASK];
             Miu[i] = mism<W>(Sm[i], U);
             hs[i] = popcm<W>(Miu[i]);
         }
@@ -132,7 +137,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         const uint32_t e = valid ? src[idx] : 0xFFFFFFFFu;
         bool keep = false;
         if (valid) {
-            const Lmer<W> V = C.T[e & ID_MASK];
+            const Lmer<W> V = C.T()[e & ID_MASK];
             const Mask<W> mu = mism<W>(V, U);
             const int hvu = popcm<W>(mu);
             keep = hvu <= two_d;
@@ -293,7 +298,7 @@ __device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k
     if (++C.pushes_since_check < 4) return;
     C.pushes_since_check = 0;
     if (!starving<W, MT>(C)) return;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     for (int kk = kmin; kk <= k; ++kk) {
         const int it = S.iter[kk], end = S.iter_end[kk];
         if (end - it >= 2) {
@@ -383,15 +388,15 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
     int n = ncand;
     unsigned long long vcmp = 0;
     for (int r = 0; r < L.nrows && n > 0; ++r) {
-        const int j = C.S->vorder[r];
+        const int j = C.S()->vorder[r];
         const int st = L.start[j], cnt = L.cnt[j];
         int scanned = 0, out = 0;
         switch ((n + 31) >> 5) {
-            case 1: out = verify_row<W, 1>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
-            case 2: out = verify_row<W, 2>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
-            case 3: out = verify_row<W, 3>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
-            case 4: out = verify_row<W, 4>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
-            default: out = verify_row<W, 5>(C.T, C.cand, entries, st, cnt, n, d, lane, scanned); break;
+            case 1: out = verify_row<W, 1>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            case 2: out = verify_row<W, 2>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            case 3: out = verify_row<W, 3>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            case 4: out = verify_row<W, 4>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            default: out = verify_row<W, 5>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
         }
         vcmp += static_cast<unsigned long long>(n) * scanned;
         n = out;
@@ -408,7 +413,7 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
             const unsigned long long pos = pos0 + __popc(em & lanemask_lt());
             if (static_cast<long long>(pos) < P.key_cap) {
                 unsigned long long klo, khi;
-                make_key<W>(C.cand[base + lane], P.l, klo, khi);
+                make_key<W>(C.cand()[base + lane], P.l, klo, khi);
                 P.keys[2 * pos] = klo;
                 P.keys[2 * pos + 1] = khi;
             }
@@ -427,7 +432,7 @@ template <int W, int MT>
 __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const LevelMeta& L, Lmer<W>* Tm) {
     const SearchParams& P = *C.P;
     const int lane = C.lane, l = P.l;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     const int np = P.plan.npair, ntot = P.plan.npair + P.plan.ntri;
     for (int p = lane; p <= l; p += 32) {
         uint32_t e = 0;
@@ -437,7 +442,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
                 if (i < t) e |= 1u << (8 * code_at<W>(Tm[i], p) + i);
             S.eq[p] = e;
         }
-        uint8_t* row = C.thr + p * ntot;
+        uint8_t* row = C.thr() + p * ntot;
 #pragma unroll
         for (int j = 1; j < MT; ++j)
 #pragma unroll
@@ -499,7 +504,7 @@ template <int W, int MT>
 __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node<W>& nd, int c, int t, uint32_t tmask,
                                              int prune, Node<W>& ch, bool& leaf) {
     const SearchParams& P = *C.P;
-    const WarpFixed& S = *C.S;
+    const WarpFixed& S = *C.S();
     const int p = static_cast<int>(nd.rB >> 24);
     const uint32_t em = (S.eq[p] >> (8 * c)) & tmask;  // members matching symbol c
     const uint32_t mm = ~em & tmask;                   // members charged on this edge
@@ -524,7 +529,7 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
         ok = true;
     } else {
         ok = !neg;
-        const uint8_t* row = C.thr + q * (P.plan.npair + P.plan.ntri);
+        const uint8_t* row = C.thr() + q * (P.plan.npair + P.plan.ntri);
         if (ok) {
 #pragma unroll
             for (int j = 1; j < MT; ++j)
@@ -578,9 +583,9 @@ __device__ __forceinline__ bool bytes_ge(uint32_t x, uint32_t y) {
 template <int W, int MT>
 __device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const LevelMeta& L, const Lmer<W>* Tm) {
     const int lane = C.lane, l = C.P->l;
-    WarpFixed& S = *C.S;
-    uint32_t* dec = reinterpret_cast<uint32_t*>(C.thr);          // [l][4]
-    uint4* thr = reinterpret_cast<uint4*>(C.thr + 16 * ((l + 3) & ~3) );  // [l+1]
+    WarpFixed& S = *C.S();
+    uint32_t* dec = reinterpret_cast<uint32_t*>(C.thr());          // [l][4]
+    uint4* thr = reinterpret_cast<uint4*>(C.thr() + 16 * ((l + 3) & ~3) );  // [l+1]
     const int nchunk = (l + 32) / 32;  // positions 0..l
     int carry = 0, carry_next = 0;
     for (int ch = nchunk - 1; ch >= 0; --ch) {
@@ -690,8 +695,8 @@ template <int W, int MT>
 __device__ __forceinline__ bool expand_child_swar(const WarpCtx<W, MT>& C, const Node<W>& nd, int c, int prune,
                                                   Node<W>& ch, bool& leaf) {
     const int l = C.P->l;
-    const uint32_t* dec = reinterpret_cast<const uint32_t*>(C.thr);
-    const uint4* thr = reinterpret_cast<const uint4*>(C.thr + 16 * ((l + 3) & ~3));
+    const uint32_t* dec = reinterpret_cast<const uint32_t*>(C.thr());
+    const uint4* thr = reinterpret_cast<const uint4*>(C.thr() + 16 * ((l + 3) & ~3));
     const int p = static_cast<int>(nd.rB >> 24);
     const uint32_t D = dec[4 * p + c];
     uint32_t R = (nd.rA | 0x80808080u) - D;
@@ -761,14 +766,14 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                                             unsigned long long& leaves_out) {
     const SearchParams& P = *C.P;
     const int lane = C.lane, l = P.l;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     constexpr int NS = NodeSmem<1>::N;
     constexpr int SPILL = NS / 4;
-    uint4* ns = reinterpret_cast<uint4*>(C.node_smem);
+    uint4* ns = reinterpret_cast<uint4*>(C.node_smem());
     uint4* ov = reinterpret_cast<uint4*>(C.node_glob);
-    uint2* cand = reinterpret_cast<uint2*>(C.cand);
-    const uint2* dec2 = reinterpret_cast<const uint2*>(C.thr);
-    const uint4* thr = reinterpret_cast<const uint4*>(C.thr + 16 * ((l + 3) & ~3));
+    uint2* cand = reinterpret_cast<uint2*>(C.cand());
+    const uint2* dec2 = reinterpret_cast<const uint2*>(C.thr());
+    const uint4* thr = reinterpret_cast<const uint4*>(C.thr() + 16 * ((l + 3) & ~3));
     const int prune = P.prune;
     const int cand_cap = P.plan.cand_cap;
     const uint32_t odd = lane & 1;
@@ -797,7 +802,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                 nov -= NDON;
             } else {
                 const int b0 = bot;
-                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem[(b0 + x) & (NS - 1)]; });
+                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem()[(b0 + x) & (NS - 1)]; });
                 bot = (bot + NDON) & (NS - 1);
                 nn -= NDON;
             }
@@ -878,7 +883,7 @@ template <int W, int MT>
 __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon) {
     const SearchParams& P = *C.P;
     const int lane = C.lane;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     const LevelMeta& L = S.lev[t];
     const uint32_t* entries = level_entries<W, MT>(C, t);
     const long long c0 = clock64();
@@ -886,7 +891,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
     Lmer<W> Tm[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
-        if (i < t) Tm[i] = C.T[S.stack_id[i] & ID_MASK];
+        if (i < t) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
     const bool swar = MT <= 4 && P.d <= 31;
     if (swar) prepare_tuple_swar<W, MT>(C, t, L, Tm);
     else prepare_tuple<W, MT>(C, t, L, Tm);
@@ -897,7 +902,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
     // fills, and come back when it drains (all hot accesses are LDS/STS)
     constexpr int NS = NodeSmem<W>::N;
     constexpr int SPILL = NS / 4;
-    Node<W>* ns = C.node_smem;
+    Node<W>* ns = C.node_smem();
     Node<W>* ov = C.node_glob;
     int bot = 0, nn = 0, nov = 0;
     if (ndon > 0) {
@@ -1002,8 +1007,8 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
         const unsigned ib0 = __ballot_sync(0xffffffffu, ok0 && !leaf0);
         const unsigned ib1 = __ballot_sync(0xffffffffu, ok1 && !leaf1);
         const unsigned lt = lanemask_lt();
-        if (ok0 && leaf0) C.cand[ncand + __popc(lb0 & lt)] = ch0.c;
-        if (ok1 && leaf1) C.cand[ncand + __popc(lb0) + __popc(lb1 & lt)] = ch1.c;
+        if (ok0 && leaf0) C.cand()[ncand + __popc(lb0 & lt)] = ch0.c;
+        if (ok1 && leaf1) C.cand()[ncand + __popc(lb0) + __popc(lb1 & lt)] = ch1.c;
         const int nl = __popc(lb0) + __popc(lb1);
         if (ok0 && !leaf0) ns[(bot + base + __popc(ib0 & lt)) & (NS - 1)] = ch0;
         if (ok1 && !leaf1) ns[(bot + base + __popc(ib0) + __popc(ib1 & lt)) & (NS - 1)] = ch1;
@@ -1030,7 +1035,7 @@ done:
 template <int W, int MT>
 __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
     const SearchParams& P = *C.P;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     const int t = P.t;
     if (C.lane == 0) {
         S.iter[kmin] = it0;
@@ -1071,7 +1076,7 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
 template <int W, int MT>
 __device__ void begin_anchor(WarpCtx<W, MT>& C, int ai) {
     const SearchParams& P = *C.P;
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     C.anchor = ai;
     C.l1 = P.l1_entries + static_cast<size_t>(ai) * P.K;
     const uint32_t* src = reinterpret_cast<const uint32_t*>(P.l1_meta + ai);
@@ -1085,32 +1090,30 @@ __device__ void begin_anchor(WarpCtx<W, MT>& C, int ai) {
 
 template <int W, int MT>
 __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ SearchParams P) {
-    extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    Lmer<W>* T = reinterpret_cast<Lmer<W>*>(smem);
+    Lmer<W>* T = reinterpret_cast<Lmer<W>*>(dyn_smem);
     const Lmer<W>* gT = static_cast<const Lmer<W>*>(P.table);
     for (int i = threadIdx.x; i < P.K; i += blockDim.x) T[i] = gT[i];
-    const size_t table_bytes = (static_cast<size_t>(P.K) * sizeof(Lmer<W>) + 15) / 16 * 16;
-    uint8_t* wbase = smem + table_bytes + static_cast<size_t>(P.plan.bytes) * warp;
+    const uint32_t table_bytes = (static_cast<uint32_t>(P.K) * sizeof(Lmer<W>) + 15u) / 16u * 16u;
+    const uint32_t wbase = table_bytes + static_cast<uint32_t>(P.plan.bytes) * warp;
     __syncthreads();
 
     WarpCtx<W, MT> C;
     C.P = &P;
-    C.T = T;
-    C.S = reinterpret_cast<WarpFixed*>(wbase);
-    C.thr = wbase + P.plan.off_thr;
-    C.cand = reinterpret_cast<Lmer<W>*>(wbase + P.plan.off_cand);
-    C.node_smem = reinterpret_cast<Node<W>*>(wbase + P.plan.off_nodes);
+    C.off_S = wbase;
+    C.off_thr = wbase + P.plan.off_thr;
+    C.off_cand = wbase + P.plan.off_cand;
+    C.off_nodes = wbase + P.plan.off_nodes;
     const size_t gw = static_cast<size_t>(blockIdx.x) * nwarps + warp;
     uint32_t* scratch = P.scratch + gw * P.scratch_words;
     C.lvl_glob = scratch;
     C.node_glob = reinterpret_cast<Node<W>*>(scratch + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap);
     C.lane = lane;
     C.pushes_since_check = 0;
-    if (lane < 16) C.S->ctr[lane] = 0;
+    if (lane < 16) C.S()->ctr[lane] = 0;
     __syncwarp();
-    WarpFixed& S = *C.S;
+    WarpFixed& S = *C.S();
     const int t = P.t;
     const unsigned long long nstatic = static_cast<unsigned long long>(P.task_base[P.nanchors]);
     QueueState* qs = P.qs;
@@ -1207,7 +1210,7 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
                     uint32_t* w = reinterpret_cast<uint32_t*>(&nd);
 #pragma unroll
                     for (int q = 0; q < NW; ++q) w[q] = __ldcg(src + x * NW + q);
-                    C.node_smem[x] = nd;
+                    C.node_smem()[x] = nd;
                 }
             }
             __syncwarp();
