@@ -53,6 +53,9 @@ typedef struct pms8g_options {
     int nanchors;
     int warps_per_block;   /* 0: default */
     int blocks_per_sm;     /* 0: default */
+    int exact_tree;        /* 1: filter every row at every push, exactly like the reference (same
+                              search tree and counters); 0 (default): the rows of the final level
+                              are filtered on demand by verification (same motif set, less work) */
 } pms8g_options;
 
 /* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */

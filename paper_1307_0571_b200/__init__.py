@@ -188,6 +188,7 @@ class ParallelOptions:
     anchors: Optional[Sequence[int]] = None
     warps_per_block: int = 0
     blocks_per_sm: int = 0
+    exact_tree: bool = False  # True: same search tree as the reference (every row filtered at every push)
 
 
 @dataclasses.dataclass
@@ -266,6 +267,7 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions]):
     o.shard_count = int(par.shard_count)
     o.warps_per_block = int(par.warps_per_block)
     o.blocks_per_sm = int(par.blocks_per_sm)
+    o.exact_tree = 1 if par.exact_tree else 0
     keep = None
     if par.anchors is not None:
         keep = np.ascontiguousarray(np.asarray(par.anchors, np.int32))

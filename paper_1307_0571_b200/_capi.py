@@ -31,6 +31,7 @@ class Options(ctypes.Structure):
         ("nanchors", ctypes.c_int),
         ("warps_per_block", ctypes.c_int),
         ("blocks_per_sm", ctypes.c_int),
+        ("exact_tree", ctypes.c_int),
     ]
 
 

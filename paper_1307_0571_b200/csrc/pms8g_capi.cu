@@ -552,7 +552,7 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
            c->opt.reverify == o.reverify && c->opt.max_motifs == o.max_motifs &&
            c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
            (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && c->opt.warps_per_block == o.warps_per_block &&
-           c->opt.blocks_per_sm == o.blocks_per_sm;
+           c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree;
 }
 }  // namespace
 
@@ -669,6 +669,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.qcap = c->qcap;
         P.qslot_bytes = c->qslot_bytes;
         P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
+        P.lazy = c->opt.exact_tree ? 0 : 1;
         P.plan = c->plan;
         P.scratch = c->d_scratch;
         P.scratch_words = c->scratch_words;

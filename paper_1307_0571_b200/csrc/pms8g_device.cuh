@@ -103,6 +103,7 @@ struct SearchParams {
     unsigned int* qstate;         // [qcap] slot round state (2r free, 2r+1 published)
     int qcap, qslot_bytes;
     int donate;                   // 1: donate work to idle warps
+    int lazy;                     // 1: rows of the final level are filtered on demand
     uint32_t* scratch;            // per-warp level storage + node stack
     size_t scratch_words;         // uint32 words per warp
     int level_cap;                // entries per level buffer

@@ -53,6 +53,8 @@ struct WarpFixed {
     uint8_t cons[68];
     TaskHeader task;
     unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
+    uint32_t lazy_mask;          // rows of the lazy level already filtered
+    int lazy_level;              // level whose rows are filtered on demand (0: none)
 };
 
 enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
@@ -126,6 +128,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const int n_iter = Ls.total - bcnt;
     const int nrows = Ls.nrows;
     if (lane < MAXN) S.cnt_by_row[lane] = 0;
+    if (lane == 0) S.lazy_level = 0;
     __syncwarp();
     int out = 0;
     bool dead = false;
@@ -237,6 +240,116 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         }
     }
     __syncwarp();
+    C.add(W_CLKF, static_cast<unsigned long long>(clock64() - f0));
+    return ok;
+}
+
+// Filter one row j of level k against u = stack[k] with the same pair +
+// Theorem-1 rule as filter_push, writing the survivors of level k+1 at the
+// row's level-k offset. Returns the surviving count.
+template <int W, int MT>
+__device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
+    const SearchParams& P = *C.P;
+    const int lane = C.lane;
+    WarpFixed& S = *C.S();
+    const LevelMeta& Ls = S.lev[k];
+    const uint32_t* src = level_entries<W, MT>(C, k) + Ls.start[j];
+    uint32_t* dst = level_entries<W, MT>(C, k + 1) + Ls.start[j];
+    const int cnt = Ls.cnt[j];
+    const int d = P.d, six_d = 6 * d, two_d = 2 * d;
+    const Lmer<W> U = C.T()[S.stack_id[k] & ID_MASK];
+    Lmer<W> Sm[MT];
+    Mask<W> Miu[MT];
+    int hs[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        if (i < k) {
+            Sm[i] = C.T()[S.stack_id[i] & ID_MASK];
+            Miu[i] = mism<W>(Sm[i], U);
+            hs[i] = popcm<W>(Miu[i]);
+        }
+    }
+    int out = 0;
+    for (int base = 0; base < cnt; base += 32) {
+        const int f = base + lane;
+        bool keep = false;
+        uint32_t e = 0;
+        if (f < cnt) {
+            e = src[f];
+            const Lmer<W> V = C.T()[e & ID_MASK];
+            const Mask<W> mu = mism<W>(V, U);
+            const int hvu = popcm<W>(mu);
+            keep = hvu <= two_d;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                if (i < k && keep) {
+                    const Mask<W> mi = mism<W>(V, Sm[i]);
+                    const int hvi = popcm<W>(mi);
+                    const int sum = hvi + hvu + hs[i];
+                    const int mn = min(min(hvi, hvu), hs[i]);
+                    keep = sum <= six_d && (sum + mn <= six_d || sum + popc_and3<W>(mi, mu, Miu[i]) <= six_d);
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
+        out += __popc(bal);
+    }
+    C.add(W_SLOTS, static_cast<unsigned long long>(cnt));
+    __syncwarp();
+    return out;
+}
+
+// Push of u = stack[k] that completes the t-tuple: instead of filtering
+// every remaining row (most are never read, because verification stops at
+// the first row without a witness), the rows of level k+1 are filtered on
+// demand by verification; only the smallest row is filtered eagerly as the
+// viability check (an empty row means no motif below, src/solver.cpp:331-334).
+template <int W, int MT>
+__device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
+    const int lane = C.lane;
+    WarpFixed& S = *C.S();
+    const LevelMeta& Ls = S.lev[k];
+    LevelMeta& Ld = S.lev[k + 1];
+    const int jb = Ls.branch;
+    const int nr2 = Ls.nrows - 1;
+    const long long f0 = clock64();
+    int c = 0x7FFF;
+    if (lane < nr2) {
+        const int j = lane < jb ? lane : lane + 1;
+        Ld.start[lane] = Ls.start[j];
+        c = Ls.cnt[j];
+        Ld.cnt[lane] = static_cast<uint16_t>(c);
+        Ld.order[lane] = Ls.order[j];
+    }
+    // smallest unfiltered row (ties by position)
+    int key = lane < nr2 ? (c << 8) | lane : 0x7FFFFFFF;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, sh));
+    if (lane == 0) {
+        Ld.nrows = nr2;
+        Ld.total = Ls.total;
+        Ld.branch = 0;
+        Ld.viable = 1;
+        S.lazy_mask = 0u;
+        S.lazy_level = k + 1;
+    }
+    __syncwarp();
+    C.add(W_PUSH, 1);
+    bool ok = true;
+    if (nr2 > 0) {
+        // the level-(k+1) row at position p comes from level-k position p' (p' skips the branch row)
+        const int p = key & 0xFF;
+        const int pk = p < jb ? p : p + 1;
+        const int got = filter_one_row<W, MT>(C, k, pk);
+        if (lane == 0) {
+            Ld.cnt[p] = static_cast<uint16_t>(got);
+            S.lazy_mask = 1u << p;
+        }
+        __syncwarp();
+        ok = got > 0;
+    }
+    if (ok) C.add(W_VIABLE, 1);
     C.add(W_CLKF, static_cast<unsigned long long>(clock64() - f0));
     return ok;
 }
@@ -377,6 +490,22 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
     return out;
 }
 
+// Make row position p of the lazy level t available (filter it on demand).
+template <int W, int MT>
+__device__ __forceinline__ void ensure_row(WarpCtx<W, MT>& C, int t, int p) {
+    WarpFixed& S = *C.S();
+    if (S.lazy_level != t || (S.lazy_mask >> p) & 1u) return;
+    const int k = t - 1;
+    const int jb = S.lev[k].branch;
+    const int pk = p < jb ? p : p + 1;
+    const int got = filter_one_row<W, MT>(C, k, pk);
+    if (C.lane == 0) {
+        S.lev[t].cnt[p] = static_cast<uint16_t>(got);
+        S.lazy_mask |= 1u << p;
+    }
+    __syncwarp();
+}
+
 // Breadth-first verification of the buffered candidates against the level's
 // rows, smallest row first (verify_candidate checks rows in size order and
 // stops at the first row without a witness); survivors are emitted as keys.
@@ -387,8 +516,10 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
     const int d = P.d;
     int n = ncand;
     unsigned long long vcmp = 0;
+    const int tlev = static_cast<int>(&L - C.S()->lev);
     for (int r = 0; r < L.nrows && n > 0; ++r) {
         const int j = C.S()->vorder[r];
+        ensure_row<W, MT>(C, tlev, j);
         const int st = L.start[j], cnt = L.cnt[j];
         int scanned = 0, out = 0;
         switch ((n + 31) >> 5) {
@@ -1058,7 +1189,8 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         }
         __syncwarp();
         maybe_donate_dfs<W, MT>(C, kmin, k);
-        if (!filter_push<W, MT>(C, k)) continue;
+        const bool ok = (k + 1 == t && P.lazy) ? lazy_push<W, MT>(C, k) : filter_push<W, MT>(C, k);
+        if (!ok) continue;
         if (k + 1 == t) {
             enumerate_verify<W, MT>(C, t, 0);
         } else {
@@ -1112,6 +1244,10 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
     C.lane = lane;
     C.pushes_since_check = 0;
     if (lane < 16) C.S()->ctr[lane] = 0;
+    if (lane == 0) {
+        C.S()->lazy_level = 0;
+        C.S()->lazy_mask = 0u;
+    }
     __syncwarp();
     WarpFixed& S = *C.S();
     const int t = P.t;
@@ -1225,7 +1361,7 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
             // replay the prefix pushes to rebuild levels 2..tk
             bool ok = true;
             for (int i = 1; i < tk && ok; ++i) {
-                ok = filter_push<W, MT>(C, i);
+                ok = (i + 1 == t && P.lazy) ? lazy_push<W, MT>(C, i) : filter_push<W, MT>(C, i);
                 C.add(W_REPLAYS, 1);
                 C.add(W_PUSH, ~0ull);  // replays are not new tree nodes
                 if (ok) C.add(W_VIABLE, ~0ull);

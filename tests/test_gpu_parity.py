@@ -26,8 +26,10 @@ def test_planted_13_4_full_instance(seed):
     inst = planted(13, 4, seed)
     rep = P.RunReport()
     t = g["report"]["threshold"]
-    got = P.solve(inst.problem, P.SolverConfig(threshold_override=t), rep)
+    # exact_tree: every row filtered at every push, as the reference does
+    got = P.run_parallel(inst.problem, P.SolverConfig(threshold_override=t), P.ParallelOptions(exact_tree=True), rep)
     assert got == g["motifs"]
+    assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == g["motifs"]
     assert inst.motif in got
     # at the reference's threshold the GPU explores the identical tree
     assert rep.counters.stacks_explored == g["report"]["stacks_explored"]
@@ -194,8 +196,8 @@ def test_work_queue_wraparound_keeps_every_node(monkeypatch):
     inst = planted(13, 4, 1)
     monkeypatch.setenv("PMS8G_QCAP", "16")
     rep = P.RunReport()
-    got = P.run_parallel(inst.problem, P.SolverConfig(threshold_override=2), P.ParallelOptions(warps_per_block=15),
-                         rep)
+    got = P.run_parallel(inst.problem, P.SolverConfig(threshold_override=2),
+                         P.ParallelOptions(warps_per_block=15, exact_tree=True), rep)
     assert got == g["motifs"]
     assert rep.counters.neighbors_visited == g["report"]["neighbors_visited"]
     assert rep.counters.motifs_emitted == g["report"]["motifs_emitted"]
