@@ -56,6 +56,10 @@ typedef struct pms8g_options {
     int exact_tree;        /* 1: filter every row at every push, exactly like the reference (same
                               search tree and counters); 0 (default): the rows of the final level
                               are filtered on demand by verification (same motif set, less work) */
+    const int32_t* branches; /* optional explicit depth-1 branches: nbranches pairs (S1 offset, l-mer
+                                id seq*(m-l+1)+offset of an l-mer in that S1 l-mer's branching row);
+                                the result is the motif set under those branches only */
+    int nbranches;
 } pms8g_options;
 
 /* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */

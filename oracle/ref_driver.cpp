@@ -285,7 +285,8 @@ int cmd_branch(int argc, char** argv) {
     const int l = std::atoi(argv[2]), d = std::atoi(argv[3]);
     const uint64_t seed = std::strtoull(argv[4], nullptr, 10);
     const long anchor = std::atol(argv[5]);
-    const auto idx = parse_list(argv[6]);
+    const std::string which = argv[6];
+    std::vector<long> idx = which == "planted" ? std::vector<long>{} : parse_list(which);
     const int t = argc > 7 ? std::atoi(argv[7]) : 0;
     const int threads = argc > 8 ? std::atoi(argv[8]) : 1;
     const auto inst = make(l, d, seed);
@@ -308,6 +309,13 @@ int cmd_branch(int argc, char** argv) {
         const auto live = s.rows().live(s.rows().row_at_position(1));
         brow.assign(live.begin(), live.end());
         std::printf("BRANCHROW %d %zu\n", s.rows().row_at_position(1), brow.size());
+    }
+    if (which == "planted") {
+        // the branching-row l-mer that is the planted occurrence of its sequence
+        for (size_t j = 0; j < brow.size(); ++j) {
+            const auto r = set.ref_of(brow[j]);
+            if (static_cast<int>(r.offset) == inst.positions[r.seq]) idx.push_back(static_cast<long>(j));
+        }
     }
     std::vector<std::vector<std::string>> res(idx.size());
     std::vector<double> secs(idx.size());

@@ -189,6 +189,7 @@ class ParallelOptions:
     warps_per_block: int = 0
     blocks_per_sm: int = 0
     exact_tree: bool = False  # True: same search tree as the reference (every row filtered at every push)
+    branches: Optional[Sequence] = None  # explicit depth-1 branches [(s1_offset, seq, offset), ...]
 
 
 @dataclasses.dataclass
@@ -247,7 +248,7 @@ def canonical_motif_set(motifs: Sequence[str]) -> MotifSet:
     return sorted(set(motifs))
 
 
-def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions]):
+def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions], windows: int = 0):
     config = config or SolverConfig()
     par = par or ParallelOptions()
     o = _capi.Options()
@@ -269,7 +270,15 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions]):
     o.blocks_per_sm = int(par.blocks_per_sm)
     o.exact_tree = 1 if par.exact_tree else 0
     keep = None
-    if par.anchors is not None:
+    if par.branches is not None:
+        # (S1 offset, seq, offset) -> (S1 offset, l-mer id = seq * (m-l+1) + offset)
+        if windows <= 0:
+            raise InvalidArgument("branches need the problem shape")
+        pairs = [(int(a), int(sq) * windows + int(off)) for a, sq, off in par.branches]
+        keep = np.ascontiguousarray(np.asarray(pairs, np.int32).reshape(-1))
+        o.branches = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        o.nbranches = len(pairs)
+    elif par.anchors is not None:
         keep = np.ascontiguousarray(np.asarray(par.anchors, np.int32))
         o.anchors = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         o.nanchors = int(len(keep))
@@ -281,7 +290,7 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions]):
 def _solve_codes(codes: np.ndarray, l: int, d: int, alphabet: Alphabet, config, par, report: Optional[RunReport]):
     L = _capi.lib()
     n, m = codes.shape
-    o, keep = _options(config, par)
+    o, keep = _options(config, par, m - l + 1)
     if par is not None and par.anchors is not None and len(par.anchors) == 0:
         if report is not None:
             report.n, report.m, report.l, report.d = n, m, l, d
@@ -420,7 +429,7 @@ class Context:
                  options: Optional[ParallelOptions] = None):
         self.alphabet = alphabet or Alphabet.dna()
         self.n, self.m, self.l, self.d = n, m, l, d
-        o, self._keep = _options(config, options)
+        o, self._keep = _options(config, options, m - l + 1)
         self._ptr = ctypes.c_void_p()
         err = ctypes.create_string_buffer(512)
         rc = _capi.lib().pms8g_ctx_create(n, m, l, d, self.alphabet.symbols.encode(), ctypes.byref(o),

@@ -32,6 +32,8 @@ class Options(ctypes.Structure):
         ("warps_per_block", ctypes.c_int),
         ("blocks_per_sm", ctypes.c_int),
         ("exact_tree", ctypes.c_int),
+        ("branches", ctypes.POINTER(ctypes.c_int32)),
+        ("nbranches", ctypes.c_int),
     ]
 
 

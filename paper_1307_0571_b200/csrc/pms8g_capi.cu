@@ -74,6 +74,10 @@ struct pms8g_ctx {
     std::string alphabet;
     pms8g_options opt{};
     std::vector<int32_t> anchors;
+    std::vector<int32_t> task_ai;
+    std::vector<uint32_t> task_u;
+    int32_t* d_task_ai = nullptr;
+    uint32_t* d_task_u = nullptr;
     int device = 0;
     int sms = 0;
     cudaStream_t stream = nullptr;
@@ -235,11 +239,35 @@ int pms8g_estimate_threshold(int n, int m, int l, int d, int sigma) {
 }
 
 int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
+    // The reference balances log Time_sample(t) against log Time_pattern(t)
+    // (Appendix D, src/solver.cpp:75-117). On the GPU the pattern phase costs
+    // relatively more per unit of the model (divergent DFS + verification vs
+    // bitwise filtering), so t is the smallest depth whose pattern term is at
+    // most 10^1.3 x the sample term; fitted on the five BASELINE configs
+    // (13,4)->2, (17,6)->3, (21,8)->4, (23,9)->4 measured on B200.
     if (const char* env = std::getenv("PMS8G_THRESHOLD")) {
         const int v = std::atoi(env);
         if (v >= 1) return std::min(v, n);
     }
-    return pms8g_estimate_threshold(n, m, l, d, sigma);
+    if (n < 2 || m <= l) return pms8g_estimate_threshold(n, m, l, d, sigma);
+    auto lg = [](unsigned __int128 v) { return static_cast<double>(std::log(static_cast<long double>(v))); };
+    const double log_nd = lg(nsize(l, d, sigma));
+    const double log_n2d = lg(nsize(l, std::min(2 * d, l), sigma));
+    const double log_p = log_n2d - l * std::log(static_cast<double>(sigma));
+    const double log_q = log_nd - log_n2d;
+    const double log_w = std::log(static_cast<double>(m - l + 1));
+    std::vector<double> terms;
+    for (int k = 1; k <= n; ++k) terms.push_back(k * log_w + 0.5 * k * (k - 1) * log_p);
+    const double beta = 1.3 * std::log(10.0);
+    for (int t = 2; t <= n; ++t) {
+        const double mx = *std::max_element(terms.begin(), terms.begin() + t);
+        double sum = 0;
+        for (int k = 0; k < t; ++k) sum += std::exp(terms[k] - mx);
+        const double ls = std::log(static_cast<double>(n)) + std::log(static_cast<double>(l)) + mx + std::log(sum);
+        const double lp = terms[t - 1] + log_nd + (t - 1) * log_q + std::log(static_cast<double>(l));
+        if (lp - ls <= beta) return t;
+    }
+    return n;
 }
 
 int pms8g_generate(int n, int m, int l, int d, int sigma, uint64_t seed, int exactly_d, uint8_t* codes_out,
@@ -327,7 +355,27 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     c->device = dev;
     c->sms = prop.multiProcessorCount;
     // S1 offsets of this call (split_subproblems, src/parallel.cpp:14-20), sharded
-    if (opt.anchors && opt.nanchors > 0) {
+    if (opt.branches && opt.nbranches > 0) {
+        if (t < 2) {
+            delete c;
+            return fail(err, errlen, PMS8G_ERR_INVALID, "explicit branches need a switch depth >= 2");
+        }
+        for (int i = 0; i < opt.nbranches; ++i) {
+            const int a = opt.branches[2 * i], u = opt.branches[2 * i + 1];
+            if (a < 0 || a >= c->w || u < 0 || u >= c->K) {
+                delete c;
+                return fail(err, errlen, PMS8G_ERR_INVALID, "branch (%d, %d) out of range", a, u);
+            }
+            if (std::find(c->anchors.begin(), c->anchors.end(), a) == c->anchors.end()) c->anchors.push_back(a);
+        }
+        std::sort(c->anchors.begin(), c->anchors.end());
+        for (int i = 0; i < opt.nbranches; ++i) {
+            const int a = opt.branches[2 * i];
+            c->task_ai.push_back(static_cast<int32_t>(std::lower_bound(c->anchors.begin(), c->anchors.end(), a) -
+                                                      c->anchors.begin()));
+            c->task_u.push_back(static_cast<uint32_t>(opt.branches[2 * i + 1]));
+        }
+    } else if (opt.anchors && opt.nanchors > 0) {
         for (int i = 0; i < opt.nanchors; ++i) {
             const int a = opt.anchors[i];
             if (a < 0 || a >= c->w) {
@@ -342,6 +390,8 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     }
     c->opt.anchors = nullptr;
     c->opt.nanchors = 0;
+    c->opt.branches = nullptr;
+    c->opt.nbranches = 0;
 
     auto cleanup_fail = [&](int code) {
         pms8g_ctx_destroy(c);
@@ -391,6 +441,8 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     AL(c->d_unique_count, sizeof(long long));
     AL(c->d_counters, sizeof(unsigned long long) * C_NCTR);
     AL(c->d_err, sizeof(int));
+    AL(c->d_task_ai, sizeof(int32_t) * std::max<size_t>(1, c->task_ai.size()));
+    AL(c->d_task_u, sizeof(uint32_t) * std::max<size_t>(1, c->task_u.size()));
     c->qcap = 8192;
     if (const char* q = std::getenv("PMS8G_QCAP")) c->qcap = std::max(16, std::atoi(q));  // ring stress tests
     c->qslot_bytes = static_cast<int>(task_slot_bytes(c->W));
@@ -404,6 +456,12 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
         cudaMallocHost(reinterpret_cast<void**>(&c->h_err), sizeof(int) * 4) != cudaSuccess)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate pinned host memory"));
     if ((rc2 = ensure_key_capacity(c, 1 << 14, err, errlen)) != PMS8G_OK) return cleanup_fail(rc2);
+    if (!c->task_ai.empty() &&
+        (cudaMemcpy(c->d_task_ai, c->task_ai.data(), sizeof(int32_t) * c->task_ai.size(), cudaMemcpyHostToDevice) !=
+             cudaSuccess ||
+         cudaMemcpy(c->d_task_u, c->task_u.data(), sizeof(uint32_t) * c->task_u.size(), cudaMemcpyHostToDevice) !=
+             cudaSuccess))
+        return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "branch upload failed"));
     if (na > 0 && cudaMemcpy(c->d_anchors, c->anchors.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice) !=
                       cudaSuccess)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "anchor upload failed"));
@@ -418,7 +476,7 @@ void pms8g_ctx_destroy(pms8g_ctx* c) {
     void* ptrs[] = {c->d_codes, c->d_table,      c->d_anchors,     c->d_l1,           c->d_meta,
                     c->d_task_base, c->d_task_counter, c->d_scratch, c->d_keys,   c->d_keys_sorted,
                     c->d_keys_unique, c->d_key_count, c->d_unique_count, c->d_cub, c->d_counters,
-                    c->d_err,     c->d_fail, c->d_qs, c->d_qslots, c->d_qstate};
+                    c->d_err,     c->d_fail, c->d_qs, c->d_qslots, c->d_qstate, c->d_task_ai, c->d_task_u};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -551,7 +609,8 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
            c->opt.threshold == o.threshold && c->opt.sort_rows == o.sort_rows && c->opt.prune_level == o.prune_level &&
            c->opt.reverify == o.reverify && c->opt.max_motifs == o.max_motifs &&
            c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
-           (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && c->opt.warps_per_block == o.warps_per_block &&
+           (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && o.branches == nullptr &&
+           c->opt.warps_per_block == o.warps_per_block &&
            c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree;
 }
 }  // namespace
@@ -576,7 +635,7 @@ int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* al
         cached = true;
     } else {
         if ((rc = pms8g_ctx_create(n, m, l, d, alphabet, &opt, &c, err, errlen))) return rc;
-        if (!opt.anchors) {
+        if (!opt.anchors && !opt.branches) {
             pms8g_ctx_destroy(g_cache);
             g_cache = c;
             cached = true;
@@ -663,6 +722,9 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.anchor_off = c->d_anchors;
         P.task_base = c->d_task_base;
         P.nanchors = na;
+        P.task_ai = c->d_task_ai;
+        P.task_u = c->d_task_u;
+        P.nexplicit = static_cast<long long>(c->task_u.size());
         P.qs = c->d_qs;
         P.qslots = c->d_qslots;
         P.qstate = c->d_qstate;

@@ -98,6 +98,9 @@ struct SearchParams {
     const int32_t* anchor_off;    // [nanchors]
     const long long* task_base;   // [nanchors + 1]
     int nanchors;
+    const int32_t* task_ai;       // explicit branch tasks: anchor index ...
+    const uint32_t* task_u;       // ... and depth-1 l-mer id (nexplicit > 0)
+    long long nexplicit;
     QueueState* qs;
     uint8_t* qslots;              // [qcap][qslot_bytes]
     unsigned int* qstate;         // [qcap] slot round state (2r free, 2r+1 published)

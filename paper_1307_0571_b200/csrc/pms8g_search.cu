@@ -1251,7 +1251,8 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
     __syncwarp();
     WarpFixed& S = *C.S();
     const int t = P.t;
-    const unsigned long long nstatic = static_cast<unsigned long long>(P.task_base[P.nanchors]);
+    const unsigned long long nstatic = P.nexplicit > 0 ? static_cast<unsigned long long>(P.nexplicit)
+                                                     : static_cast<unsigned long long>(P.task_base[P.nanchors]);
     QueueState* qs = P.qs;
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
     bool waiting = false;
@@ -1318,7 +1319,23 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
         if (kind < 0) continue;
         const long long task_t0 = clock64();
         C.add(W_TASKS, 1);
-        if (kind == 0) {
+        if (kind == 0 && P.nexplicit > 0) {
+            // explicit (S1 l-mer, depth-1 branch) task: locate u in the
+            // anchor's branching row (t >= 2)
+            begin_anchor<W, MT>(C, P.task_ai[idx]);
+            const uint32_t u = P.task_u[idx];
+            const LevelMeta& L1 = S.lev[1];
+            int j = -1;
+            if (L1.viable) {
+                const int st = L1.start[L1.branch], cnt = L1.cnt[L1.branch];
+                for (int b0 = 0; b0 < cnt && j < 0; b0 += 32) {
+                    const bool hit = b0 + lane < cnt && (C.l1[st + b0 + lane] & ID_MASK) == u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (bal) j = b0 + __ffs(bal) - 1;
+                }
+            }
+            if (j >= 0) dfs<W, MT>(C, 1, j, j + 1);
+        } else if (kind == 0) {
             // anchor: last a with task_base[a] <= idx
             int lo = 0, hi = P.nanchors - 1;
             while (lo < hi) {

@@ -145,7 +145,7 @@ def anchor_sample(l, d, seed, offsets, name):
 
 
 def branch_sample(l, d, seed, anchor, idx, name):
-    text = run("branch", l, d, seed, anchor, ",".join(map(str, idx)), 0, THREADS)
+    text = run("branch", l, d, seed, anchor, idx if isinstance(idx, str) else ",".join(map(str, idx)), 0, THREADS)
     branches = []
     brow = None
     for line in text.strip().split("\n"):
@@ -172,13 +172,19 @@ def main():
     elif what == "heavy23":
         anchor_sample(23, 9, 1, list(range(0, 578, 72)), "anchors_23_9.json")
     elif what == "heavyplanted":
-        # the S1 offset holding the planted occurrence (190 for seed 1), so the
+        # the S1 offset holding the planted occurrence in sequence 0, so the
         # heavy-config anchor parity includes a non-empty motif set
-        anchor_sample(21, 8, 1, [190, 189, 191], "anchors_21_8_planted.json")
-        anchor_sample(23, 9, 1, [190], "anchors_23_9_planted.json")
+        p21 = gen(21, 8, 1)[1][0]
+        p23 = gen(23, 9, 1)[1][0]
+        anchor_sample(21, 8, 1, [p21, p21 + 1], "anchors_21_8_planted.json")
+        anchor_sample(23, 9, 1, [p23], "anchors_23_9_planted.json")
     elif what == "heavy50":
         samples = [branch_sample(50, 21, 1, 0, [0, 1, 3], "x")]
         dump("branches_50_21.json", samples)
+    elif what == "heavy50planted":
+        # the planted S1 offset and the planted occurrence in its branching row
+        p50 = gen(50, 21, 1)[1][0]
+        dump("branches_50_21_planted.json", [branch_sample(50, 21, 1, p50, "planted", "x")])
     else:
         raise SystemExit("unknown part " + what)
 

@@ -201,3 +201,37 @@ def test_work_queue_wraparound_keeps_every_node(monkeypatch):
     assert got == g["motifs"]
     assert rep.counters.neighbors_visited == g["report"]["neighbors_visited"]
     assert rep.counters.motifs_emitted == g["report"]["motifs_emitted"]
+
+
+def _branch_parity(name):
+    path = os.path.join(ROOT, "tests", "golden", name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    for sample in golden(name):
+        inst = planted(sample["l"], sample["d"], sample["seed"])
+        for b in sample["branches"]:
+            got = P.run_parallel(inst.problem, P.SolverConfig(),
+                                 P.ParallelOptions(branches=[(sample["anchor"], b["seq"], b["offset"])]))
+            assert got == b["motifs"], (sample["anchor"], b)
+
+
+def test_branch_sample_50_21():
+    # two-word (l=50) path at full size, t from the GPU rule: depth-1 branches
+    # of S1 l-mer 0 as the reference computed them
+    _branch_parity("branches_50_21.json")
+
+
+def test_branch_planted_50_21():
+    _branch_parity("branches_50_21_planted.json")
+
+
+def test_anchor_planted_21_8_and_23_9():
+    _anchor_parity("anchors_21_8_planted.json", 21, 8)
+    _anchor_parity("anchors_23_9_planted.json", 23, 9)
+    g = golden("anchors_21_8_planted.json")
+    assert any(a["motifs"] for a in g["anchors"])
+
+
+def test_gpu_threshold_rule():
+    assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
+        [2, 3, 4, 4, 5]
