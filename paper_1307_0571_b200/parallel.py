@@ -42,6 +42,10 @@ def allgather_keys(local, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    out_dev = local.device
+    # gloo moves host tensors; NCCL moves device tensors over NVLink
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        local = local.cpu()
     dev = local.device
     cnt = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
@@ -53,7 +57,7 @@ def allgather_keys(local, group=None):
         pad[: local.shape[0]] = local
     bufs = [torch.zeros_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
-    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0).to(out_dev)
 
 
 def merge_keys_device(keys):
@@ -90,7 +94,7 @@ class _DeviceKeys:
     """__cuda_array_interface__ view of the library's device key buffer."""
 
     def __init__(self, ptr, count):
-        self.__cuda_array_interface__ = {"shape": (count, 2), "typestr": "<i8", "data": (ptr, True), "version": 3,
+        self.__cuda_array_interface__ = {"shape": (count, 2), "typestr": "<i8", "data": (ptr, False), "version": 3,
                                          "strides": None}
 
 
@@ -99,6 +103,9 @@ def device_keys_tensor(ptr: int, count: int):
     if count == 0:
         return torch.empty((0, 2), dtype=torch.int64, device="cuda")
     return torch.as_tensor(_DeviceKeys(ptr, count), device="cuda")
+
+
+_CTX_CACHE = {}
 
 
 def run_sharded(problem, config=None, options=None, report=None, group=None):
@@ -115,8 +122,17 @@ def run_sharded(problem, config=None, options=None, report=None, group=None):
     n, m = codes.shape
     opts = dataclasses.replace(options, shard_rank=rank, shard_count=world,
                                device=options.device if options.device >= 0 else torch.cuda.current_device())
-    ctx = Context(n, m, problem.motif_length, problem.max_mismatches, problem.alphabet, config, opts)
-    try:
+    # device contexts are cached per shape/options, like the library's own
+    # handle cache for pms8g_solve
+    key = (n, m, problem.motif_length, problem.max_mismatches, problem.alphabet.symbols, repr(config), repr(opts))
+    ctx = _CTX_CACHE.get(key)
+    if ctx is None:
+        for old in _CTX_CACHE.values():
+            old.close()
+        _CTX_CACHE.clear()
+        ctx = Context(n, m, problem.motif_length, problem.max_mismatches, problem.alphabet, config, opts)
+        _CTX_CACHE[key] = ctx
+    if True:
         ctx.load_codes(codes.ctypes.data, False)
         ctx.run()
         local_report = RunReport()
@@ -131,5 +147,3 @@ def run_sharded(problem, config=None, options=None, report=None, group=None):
             report.motif_count = len(motifs)
             report.gpus = world
         return motifs
-    finally:
-        ctx.close()

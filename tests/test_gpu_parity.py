@@ -4,6 +4,7 @@ every comparison is exact (bit-identical sorted motif lists)."""
 import json
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -235,3 +236,19 @@ def test_anchor_planted_21_8_and_23_9():
 def test_gpu_threshold_rule():
     assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
         [2, 3, 4, 4, 5]
+
+
+def test_sharded_ranks_on_one_gpu_match_golden():
+    # torchrun with 2 ranks sharing GPU 0 (keys exchanged with gloo): the
+    # per-rank shards, allgather and device merge give the full motif set
+    import sys
+    env = dict(os.environ, PMS8G_SINGLE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "13_4", "--steps", "1", "--no-cpu-baseline"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")][0]
+    out = json.loads(line)
+    assert out["n_gpus"] == 2
+    assert out["motifs"] == golden("planted_13_4.json")[0]["motifs"]
