@@ -454,20 +454,19 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
     constexpr int U = NCH <= 2 ? 8 : 4;
     bool done = false;
     for (int eb = 0; eb < cnt && !done; eb += 32) {
-        Lmer<W> mine;
-        if (eb + lane < cnt) mine = T[entries[st + eb + lane] & ID_MASK];
+        // lanes past the row's end hold a copy of its first entry, so whole
+        // blocks of U entries can be compared without bound checks (a
+        // duplicate cannot change "some entry is within d")
         const int lim = min(32, cnt - eb);
+        const Lmer<W> mine = T[entries[st + eb + (lane < lim ? lane : 0)] & ID_MASK];
         for (int x0 = 0; x0 < lim; x0 += U) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int x = x0 + u;
-                const Lmer<W> V = shfl_lmer<W>(mine, x & 31);
-                if (x < lim) {
+                const Lmer<W> V = shfl_lmer<W>(mine, (x0 + u) & 31);
 #pragma unroll
-                    for (int ch = 0; ch < NCH; ++ch) hit[ch] |= dist<W>(cd[ch], V) <= d;
-                }
+                for (int ch = 0; ch < NCH; ++ch) hit[ch] |= dist<W>(cd[ch], V) <= d;
             }
-            scanned += min(U, lim - x0);
+            scanned += U;
             bool all = true;
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) all &= hit[ch] || !alive[ch];
@@ -488,6 +487,35 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
     }
     __syncwarp();
     return out;
+}
+
+// Few candidates (n <= 12): lanes hold row entries instead, and each
+// candidate is checked against 32 entries per ballot, stopping at its first
+// witness.
+template <int W>
+__device__ __forceinline__ int verify_row_small(const Lmer<W>* T, Lmer<W>* cand, const uint32_t* entries, int st,
+                                               int cnt, int n, int d, int lane, int& scanned) {
+    unsigned pass = 0u;  // bit i: candidate i has a witness in this row
+    for (int eb = 0; eb < cnt; eb += 32) {
+        const bool have = eb + lane < cnt;
+        Lmer<W> mine;
+        if (have) mine = T[entries[st + eb + lane] & ID_MASK];
+        for (int i = 0; i < n; ++i) {
+            if ((pass >> i) & 1u) continue;
+            const Lmer<W> c = cand[i];
+            if (__ballot_sync(0xffffffffu, have && dist<W>(c, mine) <= d)) pass |= 1u << i;
+        }
+        scanned += min(32, cnt - eb);
+        if (pass == (n == 32 ? 0xffffffffu : ((1u << n) - 1u))) break;
+    }
+    // compact survivors in order
+    Lmer<W> mine;
+    const bool keep = lane < n && ((pass >> lane) & 1u);
+    if (lane < n) mine = cand[lane];
+    __syncwarp();
+    if (keep) cand[__popc(pass & lanemask_lt())] = mine;
+    __syncwarp();
+    return __popc(pass);
 }
 
 // Make row position p of the lazy level t available (filter it on demand).
@@ -522,7 +550,9 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
         ensure_row<W, MT>(C, tlev, j);
         const int st = L.start[j], cnt = L.cnt[j];
         int scanned = 0, out = 0;
-        switch ((n + 31) >> 5) {
+        if (n <= 12) {
+            out = verify_row_small<W>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned);
+        } else switch ((n + 31) >> 5) {
             case 1: out = verify_row<W, 1>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
             case 2: out = verify_row<W, 2>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
             case 3: out = verify_row<W, 3>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
