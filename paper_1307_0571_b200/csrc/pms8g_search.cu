@@ -938,57 +938,70 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     const int prune = P.prune;
     const int cand_cap = P.plan.cand_cap;
     const uint32_t odd = lane & 1;
-    unsigned long long rounds = 0, leaves = 0, nodes = 0;
+    unsigned long long leaves = 0, nodes = 0;
+    uint32_t leaves32 = 0, nodes32 = 0;
+    int rounds = 0;
     int ncand = 0;
+    const bool may_donate = P.donate != 0;
     while (nn > 0 || nov > 0) {
-        if (nn == 0) {
-            nov -= SPILL;
-            if (lane < SPILL) ns[(bot + lane) & (NS - 1)] = ov[nov + lane];
-            nn = SPILL;
-            __syncwarp();
-        }
-        if (P.donate && (++rounds & 15) == 0 && (nov >= NDON || nn >= NDON + 16) && starving<1, MT>(C)) {
-            TaskHeader h;
-            h.anchor = C.anchor;
-            h.kind = 1;
-            h.k = static_cast<int16_t>(t);
-            h.a0 = NDON;
-            h.a1 = 0;
+        // slow paths (uniform): refill from / spill to the global overflow,
+        // periodic donation check, 32-bit counter flush
+        if (nn == 0 || nn > NS - 48 || (++rounds & 15) == 0) {
+            if (nn == 0) {
+                nov -= SPILL;
+                if (lane < SPILL) ns[(bot + lane) & (NS - 1)] = ov[nov + lane];
+                nn = SPILL;
+                __syncwarp();
+            }
+            if ((rounds & 15) == 0) {
+                leaves += leaves32;
+                nodes += nodes32;
+                leaves32 = nodes32 = 0;
+                if (may_donate && (nov >= NDON || nn >= NDON + 16) && starving<1, MT>(C)) {
+                    TaskHeader h;
+                    h.anchor = C.anchor;
+                    h.kind = 1;
+                    h.k = static_cast<int16_t>(t);
+                    h.a0 = NDON;
+                    h.a1 = 0;
 #pragma unroll
-            for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
-            h.pad[0] = h.pad[1] = 0;
-            if (nov >= NDON) {
-                const int o0 = nov - NDON;
-                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_glob[o0 + x]; });
-                nov -= NDON;
-            } else {
-                const int b0 = bot;
-                publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem()[(b0 + x) & (NS - 1)]; });
-                bot = (bot + NDON) & (NS - 1);
-                nn -= NDON;
+                    for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
+                    h.pad[0] = h.pad[1] = 0;
+                    if (nov >= NDON) {
+                        const int o0 = nov - NDON;
+                        publish<1, MT>(C, h, NDON, [&](int x) { return C.node_glob[o0 + x]; });
+                        nov -= NDON;
+                    } else {
+                        const int b0 = bot;
+                        publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem()[(b0 + x) & (NS - 1)]; });
+                        bot = (bot + NDON) & (NS - 1);
+                        nn -= NDON;
+                    }
+                    ++rounds;
+                    continue;
+                }
             }
-            continue;
-        }
-        bool overflow = false;
-        while (nn > NS - 48) {
-            if (nov + SPILL > P.node_cap) {
-                if (lane == 0) atomicOr(P.error_flag, 2);
-                overflow = true;
-                break;
+            bool overflow = false;
+            while (nn > NS - 48) {
+                if (nov + SPILL > P.node_cap) {
+                    if (lane == 0) atomicOr(P.error_flag, 2);
+                    overflow = true;
+                    break;
+                }
+                if (lane < SPILL) ov[nov + lane] = ns[(bot + lane) & (NS - 1)];
+                nov += SPILL;
+                bot = (bot + SPILL) & (NS - 1);
+                nn -= SPILL;
+                __syncwarp();
             }
-            if (lane < SPILL) ov[nov + lane] = ns[(bot + lane) & (NS - 1)];
-            nov += SPILL;
-            bot = (bot + SPILL) & (NS - 1);
-            nn -= SPILL;
-            __syncwarp();
+            if (overflow) break;
         }
-        if (overflow) break;
         const int take = min(16, nn);
         const int base = nn - take;
         const bool active = (lane >> 1) < take;
         uint4 nd = make_uint4(0u, 0u, 0u, 0u);
         if (active) nd = ns[(bot + base + (lane >> 1)) & (NS - 1)];
-        nodes += take;
+        nodes32 += take;
         const int p = static_cast<int>(nd.w >> 24);
         const uint2 D = dec2[2 * p + odd];
         const uint4 T = thr[p + 1];
@@ -1006,7 +1019,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
         const uint32_t bit = 1u << p;
         const uint32_t h = nd.x | (odd ? bit : 0u);
         const uint32_t o1 = nd.y | bit;
-        const uint32_t q24 = static_cast<uint32_t>(p + 1) << 24;
+        const uint32_t q24 = nd.w + (1u << 24);
         __syncwarp();
         const unsigned lt = lanemask_lt();
         const unsigned lb0 = __ballot_sync(0xffffffffu, ok0 && leaf);
@@ -1014,17 +1027,18 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
         const unsigned ib0 = __ballot_sync(0xffffffffu, ok0 && !leaf);
         const unsigned ib1 = __ballot_sync(0xffffffffu, ok1 && !leaf);
         const int n0 = __popc(ib0);
-        if (ok0) {
-            if (leaf) cand[ncand + __popc(lb0 & lt)] = make_uint2(h, nd.y);
-            else ns[(bot + base + __popc(ib0 & lt)) & (NS - 1)] = make_uint4(h, nd.y, R0, q24);
+        const int nl0 = __popc(lb0);
+        if (leaf) {
+            if (ok0) cand[ncand + __popc(lb0 & lt)] = make_uint2(h, nd.y);
+            if (ok1) cand[ncand + nl0 + __popc(lb1 & lt)] = make_uint2(h, o1);
+        } else {
+            const int b2 = bot + base;
+            if (ok0) ns[(b2 + __popc(ib0 & lt)) & (NS - 1)] = make_uint4(h, nd.y, R0, q24);
+            if (ok1) ns[(b2 + n0 + __popc(ib1 & lt)) & (NS - 1)] = make_uint4(h, o1, R1, q24);
         }
-        if (ok1) {
-            if (leaf) cand[ncand + __popc(lb0) + __popc(lb1 & lt)] = make_uint2(h, o1);
-            else ns[(bot + base + n0 + __popc(ib1 & lt)) & (NS - 1)] = make_uint4(h, o1, R1, q24);
-        }
-        const int nl = __popc(lb0) + __popc(lb1);
+        const int nl = nl0 + __popc(lb1);
         ncand += nl;
-        leaves += nl;
+        leaves32 += nl;
         nn = base + n0 + __popc(ib1);
         __syncwarp();
         if (ncand > cand_cap - 64) {
@@ -1032,6 +1046,8 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
             ncand = 0;
         }
     }
+    leaves += leaves32;
+    nodes += nodes32;
     if (ncand > 0) verify_all<1, MT>(C, L, entries, ncand);
     nodes_out += nodes;
     leaves_out += leaves;
