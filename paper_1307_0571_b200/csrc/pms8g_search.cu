@@ -49,8 +49,6 @@ struct WarpFixed {
     uint32_t stack_id[MAXT];
     uint16_t cnt_by_row[MAXN];
     uint8_t vorder[MAXN];
-    uint32_t eq[64];
-    uint8_t cons[68];
     TaskHeader task;
     unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
     uint32_t lazy_mask;          // rows of the lazy level already filtered
@@ -83,6 +81,19 @@ struct WarpCtx {
         if (lane == 0) S()->ctr[i] += v;
     }
 };
+
+// generic (non-SWAR) enumeration tables at the start of the thr region:
+// eq[64] (members holding each symbol per position), cons[68] (consensus
+// suffix bound), then the pair/triple thresholds
+constexpr int GEN_TBL_BYTES = 64 * 4 + 68 + 4;
+template <int W, int MT>
+__device__ __forceinline__ uint32_t* gen_eq(const WarpCtx<W, MT>& C) {
+    return reinterpret_cast<uint32_t*>(C.thr());
+}
+template <int W, int MT>
+__device__ __forceinline__ uint8_t* gen_cons(const WarpCtx<W, MT>& C) {
+    return C.thr() + 64 * 4;
+}
 
 template <int W, int MT>
 __device__ __forceinline__ uint32_t* level_entries(WarpCtx<W, MT>& C, int k) {
@@ -601,9 +612,9 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
 #pragma unroll
             for (int i = 0; i < MT; ++i)
                 if (i < t) e |= 1u << (8 * code_at<W>(Tm[i], p) + i);
-            S.eq[p] = e;
+            gen_eq(C)[p] = e;
         }
-        uint8_t* row = C.thr() + p * ntot;
+        uint8_t* row = C.thr() + GEN_TBL_BYTES + p * ntot;
 #pragma unroll
         for (int j = 1; j < MT; ++j)
 #pragma unroll
@@ -634,7 +645,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
         const int p = ch * 32 + lane;
         int v = 0;
         if (p < l) {
-            const uint32_t e = S.eq[p];
+            const uint32_t e = gen_eq(C)[p];
             const int best = max(max(__popc(e & 0xFFu), __popc(e & 0xFF00u)),
                                  max(__popc(e & 0xFF0000u), __popc(e & 0xFF000000u)));
             v = t - best;
@@ -645,7 +656,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
             const int x = __shfl_down_sync(0xffffffffu, incl, s);
             if (lane + s < 32) incl += x;
         }
-        if (p <= l) S.cons[p] = static_cast<uint8_t>(incl + carry);
+        if (p <= l) gen_cons(C)[p] = static_cast<uint8_t>(incl + carry);
         carry += __shfl_sync(0xffffffffu, incl, 0);
     }
     if (lane < L.nrows) {
@@ -667,7 +678,7 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
     const SearchParams& P = *C.P;
     const WarpFixed& S = *C.S();
     const int p = static_cast<int>(nd.rB >> 24);
-    const uint32_t em = (S.eq[p] >> (8 * c)) & tmask;  // members matching symbol c
+    const uint32_t em = (gen_eq(C)[p] >> (8 * c)) & tmask;  // members matching symbol c
     const uint32_t mm = ~em & tmask;                   // members charged on this edge
     int r[MT];
 #pragma unroll
@@ -690,7 +701,7 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
         ok = true;
     } else {
         ok = !neg;
-        const uint8_t* row = C.thr() + q * (P.plan.npair + P.plan.ntri);
+        const uint8_t* row = C.thr() + GEN_TBL_BYTES + q * (P.plan.npair + P.plan.ntri);
         if (ok) {
 #pragma unroll
             for (int j = 1; j < MT; ++j)
@@ -712,7 +723,7 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
 #pragma unroll
             for (int i = 0; i < MT; ++i)
                 if (i < t) sum += r[i];
-            if (t >= 2) ok &= S.cons[q] <= sum;
+            if (t >= 2) ok &= gen_cons(C)[q] <= sum;
         }
     }
     uint32_t rA = 0, rB = 0;
@@ -1464,7 +1475,7 @@ WarpPlan make_plan_t(int l, int t) {
     p.ntri = tt * (tt - 1) * (tt - 2) / 6;
     int off = (static_cast<int>(sizeof(WarpFixed)) + 15) / 16 * 16;
     p.off_thr = off;
-    const int generic_thr = ((l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
+    const int generic_thr = (GEN_TBL_BYTES + (l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
     const int swar_thr = 16 * ((l + 3) & ~3) + 16 * (l + 1);
     off += generic_thr > swar_thr ? generic_thr : swar_thr;
     p.cand_cap = 32 * MAXCH;
