@@ -462,7 +462,7 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
         hit[ch] = false;
         if (alive[ch]) cd[ch] = cand[ch * 32 + lane];
     }
-    constexpr int U = NCH <= 2 ? 8 : 4;
+    constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
     bool done = false;
     for (int eb = 0; eb < cnt && !done; eb += 32) {
         // lanes past the row's end hold a copy of its first entry, so whole
@@ -566,8 +566,6 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
         } else switch ((n + 31) >> 5) {
             case 1: out = verify_row<W, 1>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
             case 2: out = verify_row<W, 2>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-            case 3: out = verify_row<W, 3>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-            case 4: out = verify_row<W, 4>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
             default: out = verify_row<W, 5>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
         }
         vcmp += static_cast<unsigned long long>(n) * scanned;
