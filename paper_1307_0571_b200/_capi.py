@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpms8g.so")
+LIB_PATH = os.environ.get("PMS8G_LIB") or os.path.join(_HERE, "lib", "libpms8g.so")
 
 PMS8G_OK, PMS8G_ERR_INVALID, PMS8G_ERR_RUNTIME, PMS8G_ERR_LOGIC, PMS8G_ERR_CUDA = range(5)
 

@@ -407,7 +407,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     // shared-memory l-mer table leaves room for
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
     c->plan = make_plan(c->W, l, t);
-    int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : 16;
+    int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
     while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) > smem_cap) --warps;
     if (search_smem(c->W, c->K, warps, c->plan) > smem_cap)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,

@@ -1275,8 +1275,12 @@ __device__ void begin_anchor(WarpCtx<W, MT>& C, int ai) {
 
 }  // namespace
 
-template <int W, int MT>
-__global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ SearchParams P) {
+// NW is the launch bound (warps per block): 16 warps x 128 registers, or for
+// the short-task l <= 32, t <= 3 searches 12 warps x 168 registers (no spills
+// in the verification pass; measured faster on (13,4) and (17,6), slower on
+// (21,8)).
+template <int W, int MT, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constant__ SearchParams P) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     Lmer<W>* T = reinterpret_cast<Lmer<W>*>(dyn_smem);
@@ -1465,6 +1469,14 @@ __global__ void __launch_bounds__(512, 1) search_kernel(const __grid_constant__ 
 
 // ---------------------------------------------------------------- host side
 
+// which (W, MT) builds also exist with the 12-warp launch bound
+template <int W, int MT>
+constexpr bool has_deep() {
+    return W == 1 && MT <= 3;
+}
+
+int search_default_warps(int W, int t) { return W == 1 && t <= 3 ? 12 : 16; }
+
 template <int W>
 WarpPlan make_plan_t(int l, int t) {
     WarpPlan p{};
@@ -1499,8 +1511,12 @@ size_t task_slot_bytes(int W) { return (sizeof(TaskHeader) + NDON * node_bytes(W
 
 template <int W, int MT>
 cudaError_t set_smem_t(size_t bytes) {
-    return cudaFuncSetAttribute(search_kernel<W, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes));
+    cudaError_t e = cudaFuncSetAttribute(search_kernel<W, MT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes));
+    if (e == cudaSuccess && has_deep<W, MT>())
+        e = cudaFuncSetAttribute(search_kernel<W, MT, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes));
+    return e;
 }
 
 // The kernel is specialised on the switch depth (tuple size) so that every
@@ -1519,7 +1535,11 @@ cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, s
     const int mt = P.t < 2 ? 2 : P.t;
 #define PMS8G_CASE(WW, M)                                                 \
     if (W == WW && mt == M) {                                             \
-        search_kernel<WW, M><<<blocks, warps * 32, smem, s>>>(P);         \
+        if (has_deep<WW, M>() && warps <= 12)                             \
+            search_kernel<WW, M, (has_deep<WW, M>() ? 12 : 16)>           \
+                <<<blocks, warps * 32, smem, s>>>(P);                     \
+        else                                                              \
+            search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P); \
         return cudaGetLastError();                                        \
     }
     PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
