@@ -732,6 +732,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.qslot_bytes = c->qslot_bytes;
         P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
         P.lazy = (c->opt.exact_tree || std::getenv("PMS8G_EAGER")) ? 0 : 1;
+        P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
         P.plan = c->plan;
         P.scratch = c->d_scratch;
         P.scratch_words = c->scratch_words;

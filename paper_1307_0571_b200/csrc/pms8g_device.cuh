@@ -107,6 +107,7 @@ struct SearchParams {
     int qcap, qslot_bytes;
     int donate;                   // 1: donate work to idle warps
     int lazy;                     // 1: rows of the final level are filtered on demand
+    int reorder;   // 1: agreement-first enumeration order (0: natural, exact_tree)
     uint32_t* scratch;            // per-warp level storage + node stack
     size_t scratch_words;         // uint32 words per warp
     int level_cap;                // entries per level buffer

@@ -49,6 +49,7 @@ struct WarpFixed {
     uint32_t stack_id[MAXT];
     uint16_t cnt_by_row[MAXN];
     uint8_t vorder[MAXN];
+    uint8_t perm[64];            // enumeration depth -> l-mer position of the current tuple
     TaskHeader task;
     unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
     uint32_t lazy_mask;          // rows of the lazy level already filtered
@@ -594,6 +595,103 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
 }
 
 // ---------------------------------------------------------------- enumeration
+// Enumeration order of the tuple's positions. The common d-neighbourhood
+// does not depend on the order in which positions are assigned, and the
+// pruning bounds of NeighborhoodEnumerator::prune (src/neighborhood.cpp:
+// 228-270) are sound for any order as long as their suffix tables follow it.
+// Positions where the members agree go first (key: consensus column cost,
+// then the number of distinct symbols; ties by position): a non-consensus
+// symbol there charges every member, so infeasible prefixes die near the
+// root (about 2x fewer tree nodes on the planted configs).
+// On return S.perm[depth] is the position assigned at that depth and Tm
+// holds the members with their symbols moved to depth order, so the suffix
+// tables can be built from Tm as if the order were natural. exact_tree keeps
+// the natural order (the reference's tree).
+template <int W, int MT>
+__device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* Tm) {
+    const int lane = C.lane, l = C.P->l;
+    WarpFixed& S = *C.S();
+    constexpr int NC = W;  // 32-position chunks
+    if (!C.P->reorder) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c * 32 + lane < l) S.perm[c * 32 + lane] = static_cast<uint8_t>(c * 32 + lane);
+        __syncwarp();
+        return;
+    }
+    int key[NC];
+    unsigned present = 0u;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int p = c * 32 + lane;
+        key[c] = 31;  // past the end: sorts last
+        if (p < l) {
+            int f[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < t) {
+                    const int ci = code_at<W>(Tm[i], p);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) f[x] += ci == x;
+                }
+            const int best = max(max(f[0], f[1]), max(f[2], f[3]));
+            const int dis = (f[0] > 0) + (f[1] > 0) + (f[2] > 0) + (f[3] > 0);
+            key[c] = (t - best) * 4 + dis - 1;
+        }
+        present |= __reduce_or_sync(0xffffffffu, 1u << key[c]);
+    }
+    int rank[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) rank[c] = 0;
+    const unsigned lt = lanemask_lt();
+    while (present) {
+        const int k = __ffs(present) - 1;
+        present &= present - 1;
+        unsigned b[NC];
+        int tot = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            b[c] = __ballot_sync(0xffffffffu, key[c] == k);
+            tot += __popc(b[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            if (key[c] > k) rank[c] += tot;
+            if (key[c] == k) {
+                int before = __popc(b[c] & lt);
+#pragma unroll
+                for (int e = 0; e < NC; ++e)
+                    if (e < c) before += __popc(b[e]);
+                rank[c] += before;
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if (c * 32 + lane < l) S.perm[rank[c]] = static_cast<uint8_t>(c * 32 + lane);
+    __syncwarp();
+    // move every member's symbols to depth order (all reads before writes)
+    uint32_t nh[MT][NC], no[MT][NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int q = c * 32 + lane;
+        const int pos = q < l ? S.perm[q] : 0;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int code = (i < t && q < l) ? code_at<W>(Tm[i], pos) : 0;
+            nh[i][c] = __ballot_sync(0xffffffffu, (code >> 1) & 1);
+            no[i][c] = __ballot_sync(0xffffffffu, code & 1);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            Tm[i].h[c] = nh[i][c];
+            Tm[i].o[c] = no[i][c];
+        }
+}
+
 // Per-tuple suffix tables (NeighborhoodEnumerator::prepare, :164-226):
 // eq[p] (members holding each symbol), pair suffix distances, Theorem-1
 // triple thresholds (Cd3 = (h_ij + h_ih + h_jh + n4) / 2 of the suffix) and
@@ -685,7 +783,7 @@ __device__ __forceinline__ bool expand_child(const WarpCtx<W, MT>& C, const Node
         r[i] = static_cast<int>((word >> (8 * (i & 3))) & 0xFFu) - 64 - static_cast<int>((mm >> i) & 1u);
     }
     ch.c = nd.c;
-    set_code<W>(ch.c, p, c);
+    set_code<W>(ch.c, S.perm[p], c);
     const int q = p + 1;
     bool neg = false;
 #pragma unroll
@@ -845,9 +943,141 @@ __device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const 
             w.x = pr[0] | (pr[1] << 8) | (pr[2] << 16) | (pr[3] << 24);
             w.y = pr[4] | (pr[5] << 8) | (cons << 16);
             w.z = tr[0] | (tr[1] << 8) | (tr[2] << 16) | (tr[3] << 24);
-            w.w = 0;
+            w.w = p >= 1 ? S.perm[p - 1] : 0u;  // position assigned by children of depth p - 1
             thr[p] = w;
         }
+    }
+    if (lane < L.nrows) {
+        const int c = L.cnt[lane];
+        int rank = 0;
+        for (int q = 0; q < L.nrows; ++q) {
+            const int cq = L.cnt[q];
+            rank += (cq < c) || (cq == c && q < lane);
+        }
+        S.vorder[rank] = static_cast<uint8_t>(lane);
+    }
+    __syncwarp();
+}
+
+// prepare_tuple_swar + order_positions for the fast loop (l <= 32, t <= 4),
+// computed on whole 32-position bit planes instead of per-position symbol
+// extraction: pair mismatch masks, Theorem-1 "all distinct" masks and the
+// consensus column-cost masks (cost >= 1, >= 2, >= 3) are a few LOP3s each,
+// every suffix sum is one shifted POPC per lane, and the agreement-first
+// order is a stable rank over at most five (cost, distinct) classes.
+template <int MT>
+__device__ __noinline__ void prepare_tuple_fast(WarpCtx<1, MT>& C, int t, const LevelMeta& L, Lmer<1>* Tm) {
+    const int lane = C.lane, l = C.P->l;
+    WarpFixed& S = *C.S();
+    uint4* dec4 = reinterpret_cast<uint4*>(C.thr());                       // [l] x {c = 0..3}
+    uint4* thr = reinterpret_cast<uint4*>(C.thr() + 16 * ((l + 3) & ~3));  // [l + 1]
+    const uint32_t lmask = l >= 32 ? 0xffffffffu : ((1u << l) - 1u);
+    const bool in = lane < l;
+    uint32_t h[MT], o[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        h[i] = i < t ? Tm[i].h[0] : 0u;
+        o[i] = i < t ? Tm[i].o[0] : 0u;
+    }
+    int pos = lane;
+    if (C.P->reorder) {
+        uint32_t e = 0;  // byte c: members holding symbol c at this lane's position
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+            if (i < t) e += 1u << (8 * ((((h[i] >> lane) & 1u) << 1) | ((o[i] >> lane) & 1u)));
+        const uint32_t m2 = __vmaxu4(e, e >> 16);
+        const int best = static_cast<int>(max(m2 & 0xFFu, (m2 >> 8) & 0xFFu));
+        const int dis = __popc((e | (e >> 1) | (e >> 2)) & 0x01010101u);
+        const int key = in ? (t - best) * 4 + dis - 1 : 31;
+        unsigned present = __reduce_or_sync(0xffffffffu, 1u << key);
+        const unsigned lt = lanemask_lt();
+        int rank = 0;
+        while (present) {
+            const int k = __ffs(present) - 1;
+            present &= present - 1;
+            const unsigned b = __ballot_sync(0xffffffffu, key == k);
+            rank += key > k ? __popc(b) : (key == k ? __popc(b & lt) : 0);
+        }
+        if (in) S.perm[rank] = static_cast<uint8_t>(lane);
+        __syncwarp();
+        pos = in ? S.perm[lane] : 0;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+            if (i < t) {
+                const uint32_t hb = __ballot_sync(0xffffffffu, in && ((h[i] >> pos) & 1u));
+                const uint32_t ob = __ballot_sync(0xffffffffu, in && ((o[i] >> pos) & 1u));
+                h[i] = hb;
+                o[i] = ob;
+            }
+    } else if (in) {
+        S.perm[lane] = static_cast<uint8_t>(lane);
+    }
+    // budget decrements of the two child pairs at this depth
+    if (in) {
+        uint32_t e = 0;  // byte c, bit i: member i holds symbol c
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+            if (i < t) e |= 1u << (8 * ((((h[i] >> lane) & 1u) << 1) | ((o[i] >> lane) & 1u)) + i);
+        const uint32_t tm = (1u << t) - 1u;
+        uint32_t dd[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dd[c] = (((~(e >> (8 * c))) & tm) * 0x00204081u) & 0x01010101u;
+        dec4[lane] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+    }
+    // suffix thresholds
+    uint32_t m[4][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = i + 1; j < MT; ++j) m[i][j] = (i < t && j < t) ? ((h[i] ^ h[j]) | (o[i] ^ o[j])) : 0u;
+    uint32_t a1 = 0u, a2 = 0u, a3 = 0u;  // column cost >= 1, >= 2, >= 3
+    if (MT == 2 || t == 2) {
+        a1 = m[0][1];
+    } else if (MT == 3 || t == 3) {
+        a1 = m[0][1] | m[0][2];
+        a2 = m[0][1] & m[0][2] & m[1][2];
+    } else if (MT >= 4 && t == 4) {
+        a1 = m[0][1] | m[0][2] | m[0][3];
+        const uint32_t three = (~m[0][1] & ~m[0][2]) | (~m[0][1] & ~m[0][3]) | (~m[0][2] & ~m[0][3]) |
+                               (~m[1][2] & ~m[1][3]);
+        a2 = ~three & lmask;
+        a3 = m[0][1] & m[0][2] & m[0][3] & m[1][2] & m[1][3] & m[2][3];
+    }
+    const int prevpos = __shfl_up_sync(0xffffffffu, pos, 1);
+    const int lastpos = __shfl_sync(0xffffffffu, pos, 31);
+    for (int q = lane; q <= l; q += 32) {
+        auto sp = [&](uint32_t x) -> uint32_t { return q < 32 ? static_cast<uint32_t>(__popc(x >> q)) : 0u; };
+        auto tri = [&](uint32_t x, uint32_t y, uint32_t z) -> uint32_t {
+            return (sp(x) + sp(y) + sp(z) + sp(x & y & z)) >> 1;
+        };
+        uint32_t pr[6] = {0u, 0u, 0u, 0u, 0u, 0u};  // 01,12,23,02,13,03
+        uint32_t tr[4] = {0u, 0u, 0u, 0u};          // 012,123,013,023
+        if (MT >= 2) pr[0] = sp(m[0][1]);
+        if (MT >= 3) {
+            pr[1] = sp(m[1][2]);
+            pr[3] = sp(m[0][2]);
+            tr[0] = tri(m[0][1], m[0][2], m[1][2]);
+        }
+        if (MT >= 4) {
+            pr[2] = sp(m[2][3]);
+            pr[4] = sp(m[1][3]);
+            pr[5] = sp(m[0][3]);
+            tr[1] = tri(m[1][2], m[1][3], m[2][3]);
+            tr[2] = tri(m[0][1], m[0][3], m[1][3]);
+            tr[3] = tri(m[0][2], m[0][3], m[2][3]);
+        }
+        // budgets are <= d <= 31 here: thresholds clamp at 127 (borrow-free compares)
+        const uint32_t cons = min(sp(a1) + sp(a2) + sp(a3), 127u);
+#pragma unroll
+        for (int x = 0; x < 6; ++x) pr[x] = min(pr[x], 127u);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) tr[x] = min(tr[x], 127u);
+        uint4 w;
+        w.x = pr[0] | (pr[1] << 8) | (pr[2] << 16) | (pr[3] << 24);
+        w.y = pr[4] | (pr[5] << 8) | (cons << 16);
+        w.z = tr[0] | (tr[1] << 8) | (tr[2] << 16) | (tr[3] << 24);
+        w.w = q == 0 ? 0u : static_cast<uint32_t>(q < 32 ? prevpos : lastpos);  // position of depth q - 1
+        thr[q] = w;
     }
     if (lane < L.nrows) {
         const int c = L.cnt[lane];
@@ -891,7 +1121,7 @@ __device__ __forceinline__ bool expand_child_swar(const WarpCtx<W, MT>& C, const
              (prune != 2 || bytes_ge(T3, T.z));
     }
     ch.c = nd.c;
-    set_code<W>(ch.c, p, c);
+    set_code<W>(ch.c, C.S()->perm[p], c);
     ch.rA = R;
     ch.rB = static_cast<uint32_t>(q) << 24;
     return ok;
@@ -1021,11 +1251,15 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
         R0 &= 0x7F7F7F7Fu;
         R1 &= 0x7F7F7F7Fu;
         const bool leaf = p + 1 == l;
-        if (!leaf && prune != 0) {
-            ok0 = ok0 && (D.x == 0u || swar_feasible<MT>(R0, T, prune));
-            ok1 = ok1 && (D.y == 0u || swar_feasible<MT>(R1, T, prune));
+        if (prune != 0) {
+            // branch-free: both children are checked on every lane (a leaf,
+            // or a child that spent no budget, is feasible by construction)
+            const bool f0 = swar_feasible<MT>(R0, T, prune);
+            const bool f1 = swar_feasible<MT>(R1, T, prune);
+            ok0 = ok0 & (leaf | (D.x == 0u) | f0);
+            ok1 = ok1 & (leaf | (D.y == 0u) | f1);
         }
-        const uint32_t bit = 1u << p;
+        const uint32_t bit = 1u << T.w;
         const uint32_t h = nd.x | (odd ? bit : 0u);
         const uint32_t o1 = nd.y | bit;
         const uint32_t q24 = nd.w + (1u << 24);
@@ -1037,14 +1271,11 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
         const unsigned ib1 = __ballot_sync(0xffffffffu, ok1 && !leaf);
         const int n0 = __popc(ib0);
         const int nl0 = __popc(lb0);
-        if (leaf) {
-            if (ok0) cand[ncand + __popc(lb0 & lt)] = make_uint2(h, nd.y);
-            if (ok1) cand[ncand + nl0 + __popc(lb1 & lt)] = make_uint2(h, o1);
-        } else {
-            const int b2 = bot + base;
-            if (ok0) ns[(b2 + __popc(ib0 & lt)) & (NS - 1)] = make_uint4(h, nd.y, R0, q24);
-            if (ok1) ns[(b2 + n0 + __popc(ib1 & lt)) & (NS - 1)] = make_uint4(h, o1, R1, q24);
-        }
+        const int b2 = bot + base;
+        if (ok0 & leaf) cand[ncand + __popc(lb0 & lt)] = make_uint2(h, nd.y);
+        if (ok1 & leaf) cand[ncand + nl0 + __popc(lb1 & lt)] = make_uint2(h, o1);
+        if (ok0 & !leaf) ns[(b2 + __popc(ib0 & lt)) & (NS - 1)] = make_uint4(h, nd.y, R0, q24);
+        if (ok1 & !leaf) ns[(b2 + n0 + __popc(ib1 & lt)) & (NS - 1)] = make_uint4(h, o1, R1, q24);
         const int nl = nl0 + __popc(lb1);
         ncand += nl;
         leaves32 += nl;
@@ -1079,8 +1310,16 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
     for (int i = 0; i < MT; ++i)
         if (i < t) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
     const bool swar = MT <= 4 && P.d <= 31;
-    if (swar) prepare_tuple_swar<W, MT>(C, t, L, Tm);
-    else prepare_tuple<W, MT>(C, t, L, Tm);
+    bool fast = false;
+    if constexpr (W == 1 && MT <= 4) fast = swar;
+    if constexpr (W == 1 && MT <= 4) {
+        if (fast) prepare_tuple_fast<MT>(C, t, L, Tm);
+    }
+    if (!fast) {
+        order_positions<W, MT>(C, t, Tm);
+        if (swar) prepare_tuple_swar<W, MT>(C, t, L, Tm);
+        else prepare_tuple<W, MT>(C, t, L, Tm);
+    }
 
     const uint32_t tmask = (1u << t) - 1u;
     // node stack: circular buffer of NS nodes in shared memory; chunks of
