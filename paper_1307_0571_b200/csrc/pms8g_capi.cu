@@ -731,6 +731,11 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.qcap = c->qcap;
         P.qslot_bytes = c->qslot_bytes;
         P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
+        P.don_pushes = 4;
+        P.don_rounds_mask = 63;
+        if (const char* e = std::getenv("PMS8G_DON_PUSHES")) P.don_pushes = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("PMS8G_LOG_CYCLES")) P.log_cycles = std::atoll(e);
+        if (const char* e = std::getenv("PMS8G_DON_ROUNDS")) P.don_rounds_mask = std::max(1, std::atoi(e)) - 1;
         P.lazy = (c->opt.exact_tree || std::getenv("PMS8G_EAGER")) ? 0 : 1;
         P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
         P.plan = c->plan;
@@ -743,6 +748,13 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.key_cap = c->key_cap;
         P.counters = c->d_counters;
         P.error_flag = c->d_err;
+        const char* tl_path = std::getenv("PMS8G_TIMELINE");  // diagnostics: task timeline dump
+        unsigned long long* d_tl = nullptr;
+        if (tl_path) {
+            P.timeline_cap = 1 << 21;
+            CU(cudaMalloc(&d_tl, sizeof(unsigned long long) * 2 * P.timeline_cap));
+            P.timeline = d_tl;
+        }
         CU(cudaEventRecord(c->ev[2], s));
         if (na > 0) CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
         CU(cudaEventRecord(c->ev[3], s));
@@ -753,6 +765,16 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         CU(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         CU(cudaGetLastError());
+        if (d_tl) {
+            const long long ntl = std::min<long long>(static_cast<long long>(c->h_counters[C_TLN]), P.timeline_cap);
+            std::vector<unsigned long long> h(2 * static_cast<size_t>(ntl));
+            CU(cudaMemcpy(h.data(), d_tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            CU(cudaFree(d_tl));
+            if (FILE* f = std::fopen(tl_path, "wb")) {
+                std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+                std::fclose(f);
+            }
+        }
         if (c->h_err[0] & 1) return fail(err, errlen, PMS8G_ERR_INVALID, "symbol code outside the 2-bit alphabet");
         if (c->h_err[0] & 2)
             return fail(err, errlen, PMS8G_ERR_RUNTIME, "enumeration stack overflow (l=%d, capacity %d nodes)", c->l,

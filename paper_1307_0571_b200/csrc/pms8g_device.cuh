@@ -50,7 +50,13 @@ enum Ctr {
     C_DONATED,    // dynamic tasks donated
     C_REPLAYS,    // filter pushes replayed by receivers of donated tasks
     C_HIST0,      // task duration histogram: C_HIST0 + floor(log2(cycles)), 40 buckets
-    C_NCTR = C_HIST0 + 40
+    C_IDLE = C_HIST0 + 40,  // warp cycles spent without a task (claim loop, incl. the final wait)
+    C_HIST_DON0,            // the same histogram for donated branch ranges (kind 0), 40 buckets
+    C_HIST_DON1 = C_HIST_DON0 + 40,  // ... and for donated node batches (kind 1)
+    C_LOGN = C_HIST_DON1 + 40,       // diagnostics: number of long tasks logged
+    C_LOG0,                          // 32 records x 8 words: kind, anchor, idx, cycles, tuples, leaves, nodes, vcmp
+    C_TLN = C_LOG0 + 256,            // diagnostics: timeline records written
+    C_NCTR
 };
 
 constexpr int NDON = 32;  // enumeration nodes per donated task
@@ -106,6 +112,11 @@ struct SearchParams {
     unsigned int* qstate;         // [qcap] slot round state (2r free, 2r+1 published)
     int qcap, qslot_bytes;
     int donate;                   // 1: donate work to idle warps
+    int don_pushes;               // DFS pushes between starvation checks
+    long long log_cycles;         // diagnostics: log tasks longer than this (0: off)
+    unsigned long long* timeline; // diagnostics: per-task {start ns, end ns | kind << 62} records (or null)
+    long long timeline_cap;
+    int don_rounds_mask;          // enumeration rounds between starvation checks - 1 (power of two - 1)
     int lazy;                     // 1: rows of the final level are filtered on demand
     int reorder;   // 1: agreement-first enumeration order (0: natural, exact_tree)
     uint32_t* scratch;            // per-warp level storage + node stack

@@ -50,6 +50,7 @@ struct WarpFixed {
     uint16_t cnt_by_row[MAXN];
     uint8_t vorder[MAXN];
     uint8_t perm[64];            // enumeration depth -> l-mer position of the current tuple
+    unsigned long long diag[5];  // diagnostics: counters at task start + start time (ns)
     TaskHeader task;
     unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
     uint32_t lazy_mask;          // rows of the lazy level already filtered
@@ -420,7 +421,7 @@ __device__ bool starving(WarpCtx<W, MT>& C) {
 template <int W, int MT>
 __device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k) {
     if (!C.P->donate) return;
-    if (++C.pushes_since_check < 4) return;
+    if (++C.pushes_since_check < C.P->don_pushes) return;
     C.pushes_since_check = 0;
     if (!starving<W, MT>(C)) return;
     WarpFixed& S = *C.S();
@@ -1185,14 +1186,14 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     while (nn > 0 || nov > 0) {
         // slow paths (uniform): refill from / spill to the global overflow,
         // periodic donation check, 32-bit counter flush
-        if (nn == 0 || nn > NS - 48 || (++rounds & 15) == 0) {
+        if (nn == 0 || nn > NS - 48 || (++rounds & P.don_rounds_mask) == 0) {
             if (nn == 0) {
                 nov -= SPILL;
                 if (lane < SPILL) ns[(bot + lane) & (NS - 1)] = ov[nov + lane];
                 nn = SPILL;
                 __syncwarp();
             }
-            if ((rounds & 15) == 0) {
+            if ((rounds & P.don_rounds_mask) == 0) {
                 leaves += leaves32;
                 nodes += nodes32;
                 leaves32 = nodes32 = 0;
@@ -1201,7 +1202,9 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                     h.anchor = C.anchor;
                     h.kind = 1;
                     h.k = static_cast<int16_t>(t);
-                    h.a0 = NDON;
+                    // the shallowest 32 nodes (overflow first)
+                    const int half = NDON;
+                    h.a0 = half;
                     h.a1 = 0;
 #pragma unroll
                     for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
@@ -1212,9 +1215,9 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                         nov -= NDON;
                     } else {
                         const int b0 = bot;
-                        publish<1, MT>(C, h, NDON, [&](int x) { return C.node_smem()[(b0 + x) & (NS - 1)]; });
-                        bot = (bot + NDON) & (NS - 1);
-                        nn -= NDON;
+                        publish<1, MT>(C, h, half, [&](int x) { return C.node_smem()[(b0 + x) & (NS - 1)]; });
+                        bot = (bot + half) & (NS - 1);
+                        nn -= half;
                     }
                     ++rounds;
                     continue;
@@ -1375,7 +1378,8 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
             h.anchor = C.anchor;
             h.kind = 1;
             h.k = static_cast<int16_t>(t);
-            h.a0 = NDON;
+            const int half = NDON;
+            h.a0 = half;
             h.a1 = 0;
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
@@ -1386,9 +1390,9 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
                 nov -= NDON;
             } else {
                 const int b0 = bot;
-                publish<W, MT>(C, h, NDON, [&](int x) { return ns[(b0 + x) & (NS - 1)]; });
-                bot = (bot + NDON) & (NS - 1);
-                nn -= NDON;
+                publish<W, MT>(C, h, half, [&](int x) { return ns[(b0 + x) & (NS - 1)]; });
+                bot = (bot + half) & (NS - 1);
+                nn -= half;
             }
             continue;
         }
@@ -1606,16 +1610,30 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             } else if (waiting) {
                 atomicSub(&qs->waiting, 1u);
                 waiting = false;
+                atomicAdd(P.counters + C_IDLE, static_cast<unsigned long long>(clock64() - wait_t0));
             }
         }
         kind = __shfl_sync(0xffffffffu, kind, 0);
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if (kind == 2) {
-            if (lane == 0 && waiting) atomicSub(&qs->waiting, 1u);
+            if (lane == 0 && waiting) {
+                atomicSub(&qs->waiting, 1u);
+                atomicAdd(P.counters + C_IDLE, static_cast<unsigned long long>(clock64() - wait_t0));
+            }
             break;
         }
         if (kind < 0) continue;
         const long long task_t0 = clock64();
+        if ((P.timeline || P.log_cycles) && lane == 0) {
+            // diagnostics only; kept in shared memory, not in registers
+            unsigned long long ns0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns0));
+            S.diag[0] = S.ctr[W_TUPLES];
+            S.diag[1] = S.ctr[W_LEAVES];
+            S.diag[2] = S.ctr[W_NODES];
+            S.diag[3] = S.ctr[W_VCMP];
+            S.diag[4] = ns0;
+        }
         C.add(W_TASKS, 1);
         if (kind == 0 && P.nexplicit > 0) {
             // explicit (S1 l-mer, depth-1 branch) task: locate u in the
@@ -1694,7 +1712,32 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             __threadfence();
             atomicSub(&qs->busy, 1u);
             const long long dt = clock64() - task_t0;
-            atomicAdd(P.counters + C_HIST0 + min(39, 63 - __clzll(dt > 0 ? dt : 1)), 1ull);
+            if (P.timeline) {
+                unsigned long long ns1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
+                const unsigned long long slot = atomicAdd(P.counters + C_TLN, 1ull);
+                if (static_cast<long long>(slot) < P.timeline_cap) {
+                    const unsigned long long kd = kind == 0 ? 0ull : 1ull + S.task.kind;
+                    P.timeline[2 * slot] = S.diag[4];
+                    P.timeline[2 * slot + 1] = ns1 | (kd << 62);
+                }
+            }
+            if ((P.log_cycles > 0 && dt > P.log_cycles) || (P.log_cycles < 0 && kind != 0 && dt > -P.log_cycles)) {
+                const unsigned long long slot = atomicAdd(P.counters + C_LOGN, 1ull);
+                if (slot < 32) {
+                    unsigned long long* r = P.counters + C_LOG0 + 8 * slot;
+                    r[0] = kind == 0 ? 0ull : 1ull + S.task.kind;
+                    r[1] = static_cast<unsigned long long>(C.anchor);
+                    r[2] = idx;
+                    r[3] = static_cast<unsigned long long>(dt);
+                    r[4] = S.ctr[W_TUPLES] - S.diag[0];
+                    r[5] = S.ctr[W_LEAVES] - S.diag[1];
+                    r[6] = S.ctr[W_NODES] - S.diag[2];
+                    r[7] = S.ctr[W_VCMP] - S.diag[3];
+                }
+            }
+            const int hb = kind == 0 ? C_HIST0 : (S.task.kind == 0 ? C_HIST_DON0 : C_HIST_DON1);
+            atomicAdd(P.counters + hb + min(39, 63 - __clzll(dt > 0 ? dt : 1)), 1ull);
         }
     }
     __syncwarp();

@@ -13,8 +13,10 @@ reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 stride = int(sys.argv[5]) if len(sys.argv) > 5 else 1
 inst = P.generate_planted_instance(P.PlantedInstanceSpec(l=l, d=d, seed=1, mutation=P.MutationMode.exactly_d))
 anchors = list(range(0, 600 - l + 1, stride)) if stride > 1 else None
+shard = os.environ.get("SHARD")  # "r/N": interleaved shard r of N
+sr, sn = (int(x) for x in shard.split("/")) if shard else (0, 1)
 ctx = P.Context(20, 600, l, d, P.Alphabet.dna(), P.SolverConfig(threshold_override=t or None),
-                P.ParallelOptions(anchors=anchors))
+                P.ParallelOptions(anchors=anchors, shard_rank=sr, shard_count=sn))
 ctx.load_codes(inst.codes.ctypes.data, False)
 for r in range(reps):
     t0 = time.perf_counter()
@@ -29,5 +31,20 @@ print(f"({l},{d}) t={rep.threshold} anchors={rep.subproblems} wall={dt*1e3:.2f}m
       f"motifs={motifs}")
 print("  " + " ".join(f"{n}={v}" for n, v in zip(names, c)))
 hist = c[15:55]
+if len(c) > 55:
+    import torch
+    props = torch.cuda.get_device_properties(0)
+    ms = ctx.kernel_ms()[0]
+    warps = 12 if (l <= 32 and rep.threshold <= 3) else 16  # search_default_warps
+    tot = props.multi_processor_count * warps * ms * 1e-3 * 1.965e9
+    for nm, lo in (("donated ranges", 56), ("donated nodes", 96)):
+        print(f"  {nm} histogram: " + " ".join(f"{i}:{v}" for i, v in enumerate(c[lo:lo + 40]) if v))
+    nlog = min(c[136], 14) if len(c) > 136 else 0
+    for i in range(nlog):
+        r = c[137 + 8 * i:145 + 8 * i]
+        print(f"  long task kind={r[0]} anchor={r[1]} idx={r[2]} cycles={r[3]:.3e} tuples={r[4]} leaves={r[5]} "
+              f"nodes={r[6]} vcmp={r[7]}")
+    print(f"  idle warp-cycles {c[55]:.3e} busy(filter+pattern) {c[8] + c[9]:.3e}"
+          + (f" of {tot:.3e} available: idle {c[55] / tot:.1%}" if tot else ""))
 print("  task cycles histogram (log2 bucket: count): " +
       " ".join(f"{i}:{v}" for i, v in enumerate(hist) if v))
