@@ -462,9 +462,9 @@ class Context:
 
     def counters(self):
         """Raw device counters of the last run (see pms8g_device.cuh Ctr)."""
-        buf = (ctypes.c_uint64 * 256)()
-        k = _capi.lib().pms8g_ctx_counters(self._ptr, buf, 256)
-        return [int(buf[i]) for i in range(min(k, 256))]
+        buf = (ctypes.c_uint64 * 512)()
+        k = _capi.lib().pms8g_ctx_counters(self._ptr, buf, 512)
+        return [int(buf[i]) for i in range(min(k, 512))]
 
     def kernel_ms(self):
         a, b = ctypes.c_float(), ctypes.c_float()

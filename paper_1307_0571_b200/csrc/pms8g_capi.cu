@@ -88,6 +88,10 @@ struct pms8g_ctx {
     uint32_t* d_l1 = nullptr;
     LevelMeta* d_meta = nullptr;
     long long* d_task_base = nullptr;
+    uint32_t* d_order = nullptr;  // static task order: keys in/out, vals in/out (4 x order_cap)
+    long long order_cap = 0;
+    void* d_order_tmp = nullptr;
+    size_t order_tmp_bytes = 0;
     unsigned long long* d_task_counter = nullptr;
     uint32_t* d_scratch = nullptr;
     size_t scratch_words = 0;
@@ -443,6 +447,15 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     AL(c->d_err, sizeof(int));
     AL(c->d_task_ai, sizeof(int32_t) * std::max<size_t>(1, c->task_ai.size()));
     AL(c->d_task_u, sizeof(uint32_t) * std::max<size_t>(1, c->task_u.size()));
+    if (c->task_u.empty() && t >= 2 && !std::getenv("PMS8G_NO_TASK_ORDER")) {
+        // heaviest-first static task order (taskorder_kernel + stable radix sort)
+        c->order_cap = static_cast<long long>(std::max(1, na)) * c->w;
+        AL(c->d_order, sizeof(uint32_t) * 4 * c->order_cap);
+        uint32_t* k0 = c->d_order;
+        cub::DeviceRadixSort::SortPairs(nullptr, c->order_tmp_bytes, k0, k0 + c->order_cap, k0 + 2 * c->order_cap,
+                                        k0 + 3 * c->order_cap, static_cast<int>(c->order_cap), 0, 8);
+        AL(c->d_order_tmp, std::max<size_t>(16, c->order_tmp_bytes));
+    }
     c->qcap = 8192;
     if (const char* q = std::getenv("PMS8G_QCAP")) c->qcap = std::max(16, std::atoi(q));  // ring stress tests
     c->qslot_bytes = static_cast<int>(task_slot_bytes(c->W));
@@ -476,7 +489,8 @@ void pms8g_ctx_destroy(pms8g_ctx* c) {
     void* ptrs[] = {c->d_codes, c->d_table,      c->d_anchors,     c->d_l1,           c->d_meta,
                     c->d_task_base, c->d_task_counter, c->d_scratch, c->d_keys,   c->d_keys_sorted,
                     c->d_keys_unique, c->d_key_count, c->d_unique_count, c->d_cub, c->d_counters,
-                    c->d_err,     c->d_fail, c->d_qs, c->d_qslots, c->d_qstate, c->d_task_ai, c->d_task_u};
+                    c->d_err,     c->d_fail, c->d_qs, c->d_qslots, c->d_qstate, c->d_task_ai, c->d_task_u,
+                    c->d_order, c->d_order_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -706,6 +720,17 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
                            c->d_meta, c->d_counters, s));
         CU(cudaEventRecord(c->ev[1], s));
         CU(launch_taskscan(c->d_meta, na, c->t, c->d_task_base, s));
+        const uint32_t* task_order = nullptr;
+        if (c->d_order && na > 0) {
+            uint32_t* k0 = c->d_order;
+            const long long oc = c->order_cap;
+            CU(launch_taskorder(c->W, c->d_table, c->d_l1, c->d_meta, c->d_anchors, c->d_task_base, na, c->K, oc, k0,
+                                k0 + 2 * oc, s));
+            size_t tb = c->order_tmp_bytes;
+            CU(cub::DeviceRadixSort::SortPairs(c->d_order_tmp, tb, k0, k0 + oc, k0 + 2 * oc, k0 + 3 * oc,
+                                               static_cast<int>(oc), 0, 8, s));
+            task_order = k0 + 3 * oc;
+        }
         SearchParams P{};
         P.n = c->n;
         P.m = c->m;
@@ -721,6 +746,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.l1_meta = c->d_meta;
         P.anchor_off = c->d_anchors;
         P.task_base = c->d_task_base;
+        P.task_order = task_order;
         P.nanchors = na;
         P.task_ai = c->d_task_ai;
         P.task_u = c->d_task_u;
@@ -733,6 +759,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
         P.don_pushes = 4;
         P.don_rounds_mask = 63;
+        P.don_burst = 1;
+        if (const char* e = std::getenv("PMS8G_DON_BURST")) P.don_burst = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PMS8G_DON_PUSHES")) P.don_pushes = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PMS8G_LOG_CYCLES")) P.log_cycles = std::atoll(e);
         if (const char* e = std::getenv("PMS8G_DON_ROUNDS")) P.don_rounds_mask = std::max(1, std::atoi(e)) - 1;

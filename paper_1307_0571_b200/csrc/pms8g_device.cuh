@@ -116,7 +116,9 @@ struct SearchParams {
     long long log_cycles;         // diagnostics: log tasks longer than this (0: off)
     unsigned long long* timeline; // diagnostics: per-task {start ns, end ns | kind << 62} records (or null)
     long long timeline_cap;
+    const uint32_t* task_order;   // static task permutation (heaviest first), or null
     int don_rounds_mask;          // enumeration rounds between starvation checks - 1 (power of two - 1)
+    int don_burst;                // node batches donated per check at most
     int lazy;                     // 1: rows of the final level are filtered on demand
     int reorder;   // 1: agreement-first enumeration order (0: natural, exact_tree)
     uint32_t* scratch;            // per-warp level storage + node stack

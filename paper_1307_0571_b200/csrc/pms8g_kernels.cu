@@ -21,6 +21,7 @@
 // popc((a.h ^ b.h) | (a.o ^ b.o)) per 32 symbols (1 LOP3-pair + POPC).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "pms8g_device.cuh"
@@ -171,6 +172,55 @@ __global__ void taskscan_kernel(const LevelMeta* __restrict__ l1_meta, int nanch
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) task_base[nanchors] = carry;
+}
+
+// ---------------------------------------------------------------------------
+// Static task order (heaviest first): task idx = (anchor a, depth-1 branch j)
+// gets the key dist(anchor, u_j). Closer pairs have far more compatible
+// l-mers below them, so sorting by the key front-loads the long tasks and
+// leaves the short ones for the end of the queue (less tail for the
+// dynamic donation to absorb). Slots past the task count sort last.
+template <int W>
+__global__ void taskorder_kernel(const Lmer<W>* __restrict__ table, const uint32_t* __restrict__ l1_entries,
+                                 const LevelMeta* __restrict__ l1_meta, const int32_t* __restrict__ anchor_off,
+                                 const long long* __restrict__ task_base, int nanchors, int K, long long cap,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const long long nstatic = task_base[nanchors];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cap;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        uint32_t key = 0xFFFFFFFFu;
+        if (i < nstatic) {
+            int lo = 0, hi = nanchors - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (task_base[mid] <= i) lo = mid;
+                else hi = mid - 1;
+            }
+            const LevelMeta& M = l1_meta[lo];
+            const int j = static_cast<int>(i - task_base[lo]);
+            const uint32_t u = l1_entries[static_cast<size_t>(lo) * K + M.start[M.branch] + j] & ID_MASK;
+            const Lmer<W> A = table[anchor_off[lo]], U = table[u];
+            int dd = 0;
+#pragma unroll
+            for (int x = 0; x < W; ++x) dd += __popc((A.h[x] ^ U.h[x]) | (A.o[x] ^ U.o[x]));
+            key = static_cast<uint32_t>(dd);
+        }
+        keys[i] = key;
+        vals[i] = static_cast<uint32_t>(i);
+    }
+}
+
+cudaError_t launch_taskorder(int W, const void* table, const uint32_t* l1_entries, const LevelMeta* l1_meta,
+                             const int32_t* anchor_off, const long long* task_base, int nanchors, int K,
+                             long long cap, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    const int blocks = static_cast<int>(std::min<long long>((cap + 255) / 256, 4096));
+    if (W == 1)
+        taskorder_kernel<1><<<blocks, 256, 0, s>>>(static_cast<const Lmer<1>*>(table), l1_entries, l1_meta,
+                                                   anchor_off, task_base, nanchors, K, cap, keys, vals);
+    else
+        taskorder_kernel<2><<<blocks, 256, 0, s>>>(static_cast<const Lmer<2>*>(table), l1_entries, l1_meta,
+                                                   anchor_off, task_base, nanchors, K, cap, keys, vals);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

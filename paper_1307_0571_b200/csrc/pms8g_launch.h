@@ -22,6 +22,9 @@ cudaError_t launch_rowbuild(int W, const void* table, int n, int w, int d, int K
                             unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_taskscan(const LevelMeta* l1_meta, int nanchors, int t, long long* task_base, cudaStream_t s);
 int search_default_warps(int W, int t);  // launch shape: 12 or 16 warps per block
+cudaError_t launch_taskorder(int W, const void* table, const uint32_t* l1_entries, const LevelMeta* l1_meta,
+                             const int32_t* anchor_off, const long long* task_base, int nanchors, int K,
+                             long long cap, uint32_t* keys, uint32_t* vals, cudaStream_t s);
 cudaError_t set_search_smem(int W, int t, size_t bytes);
 cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s);
 cudaError_t launch_reverify(int W, const void* table, int n, int w, int l, int d, const unsigned long long* keys,

@@ -144,13 +144,18 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     if (lane == 0) S.lazy_level = 0;
     __syncwarp();
     int out = 0;
-    bool dead = false;
     unsigned pair_rej = 0, tri_rej = 0;
+    // the next block's entries are loaded one iteration ahead (the level
+    // entries stream from L2; this hides one load latency per block)
+    auto load_entry = [&](int f) -> uint32_t {
+        return f < n_iter ? src[f < bstart ? f : f + bcnt] : 0xFFFFFFFFu;
+    };
+    uint32_t e_next = load_entry(lane);
     for (int base = 0; base < n_iter; base += 32) {
         const int f = base + lane;
         const bool valid = f < n_iter;
-        const int idx = f < bstart ? f : f + bcnt;
-        const uint32_t e = valid ? src[idx] : 0xFFFFFFFFu;
+        const uint32_t e = e_next;
+        e_next = load_entry(f + 32);
         bool keep = false;
         if (valid) {
             const Lmer<W> V = C.T()[e & ID_MASK];
@@ -177,29 +182,15 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
         out += __popc(bal);
-        // per-row kept counts: rows are contiguous segments of the flat range
+        // per-row kept counts: one leader lane per distinct row of the block
+        // (rows are contiguous segments, so a block spans one or two rows)
         const uint32_t row = e >> 24;
-        const uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1);
-        const uint32_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
-        const bool first = valid && (lane == 0 || prow != row);
-        const bool nvalid = (f + 1) < n_iter;
-        const bool last = valid && (lane == 31 || !nvalid || nrow != row);
-        const unsigned starts = __ballot_sync(0xffffffffu, first);
-        bool empty_row = false;
-        if (last) {
-            const int s0 = 31 - __clz(starts & ((2u << lane) - 1u));
-            const unsigned segmask = ((2u << lane) - 1u) & ~((1u << s0) - 1u);
-            const int kept = __popc(bal & segmask) + S.cnt_by_row[row];
-            S.cnt_by_row[row] = static_cast<uint16_t>(kept);
-            const bool complete = (lane < 31 && (!nvalid || nrow != row)) || (lane == 31 && !nvalid);
-            empty_row = complete && kept == 0;
-        }
+        const unsigned grp = __match_any_sync(0xffffffffu, row);
+        if (valid && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint16_t>(__popc(bal & grp));
         __syncwarp();
-        if (__any_sync(0xffffffffu, empty_row)) {
-            dead = true;
-            break;
-        }
     }
+    // an emptied row is detected after the pass (almost every push is viable,
+    // so the pass rarely could have stopped early)
     C.add(W_PUSH, 1);
     C.add(W_SLOTS, static_cast<unsigned long long>(n_iter));
     {
@@ -212,8 +203,8 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         C.add(W_PAIRREJ, pr);
         C.add(W_TRIREJ, tr);
     }
-    bool ok = !dead;
-    if (ok) {
+    bool ok = true;
+    {
         const int nr2 = nrows - 1;
         int c = 0;
         uint8_t row = 0;
@@ -283,12 +274,13 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
         }
     }
     int out = 0;
+    uint32_t e_next = lane < cnt ? src[lane] : 0u;  // one block ahead
     for (int base = 0; base < cnt; base += 32) {
         const int f = base + lane;
         bool keep = false;
-        uint32_t e = 0;
+        const uint32_t e = e_next;
+        e_next = f + 32 < cnt ? src[f + 32] : 0u;
         if (f < cnt) {
-            e = src[f];
             const Lmer<W> V = C.T()[e & ID_MASK];
             const Mask<W> mu = mism<W>(V, U);
             const int hvu = popcm<W>(mu);
@@ -1180,7 +1172,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     const uint32_t odd = lane & 1;
     unsigned long long leaves = 0, nodes = 0;
     uint32_t leaves32 = 0, nodes32 = 0;
-    int rounds = 0;
+    int rounds = 0, burst = 0;
     int ncand = 0;
     const bool may_donate = P.donate != 0;
     while (nn > 0 || nov > 0) {
@@ -1219,9 +1211,12 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                         bot = (bot + half) & (NS - 1);
                         nn -= half;
                     }
-                    ++rounds;
+                    // up to don_burst donations per check while warps starve
+                    if (++burst < P.don_burst) --rounds;
+                    else burst = 0;
                     continue;
                 }
+                burst = 0;
             }
             bool overflow = false;
             while (nn > NS - 48) {
@@ -1652,6 +1647,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             }
             if (j >= 0) dfs<W, MT>(C, 1, j, j + 1);
         } else if (kind == 0) {
+            if (P.task_order) idx = P.task_order[idx];
             // anchor: last a with task_base[a] <= idx
             int lo = 0, hi = P.nanchors - 1;
             while (lo < hi) {
@@ -1688,16 +1684,26 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                 atomicExch(&P.qstate[idx % qcap], 2u * static_cast<unsigned int>(idx / qcap) + 2u);
             }
             const int tk = S.task.k;
+            long long tdiag[3] = {0, 0, 0};
+            if (P.log_cycles) tdiag[0] = clock64() - task_t0;
             begin_anchor<W, MT>(C, S.task.anchor);
             if (lane < MAXT && lane >= 1 && lane < tk) S.stack_id[lane] = S.task.stack[lane];
             __syncwarp();
+            if (P.log_cycles) tdiag[1] = clock64() - task_t0;
             // replay the prefix pushes to rebuild levels 2..tk
             bool ok = true;
             for (int i = 1; i < tk && ok; ++i) {
                 ok = (i + 1 == t && P.lazy) ? lazy_push<W, MT>(C, i) : filter_push<W, MT>(C, i);
+                if (P.log_cycles && i == 1) tdiag[2] = clock64() - task_t0;
                 C.add(W_REPLAYS, 1);
                 C.add(W_PUSH, ~0ull);  // replays are not new tree nodes
                 if (ok) C.add(W_VIABLE, ~0ull);
+            }
+            if (P.log_cycles && lane == 0) {
+                S.diag[3] = static_cast<unsigned long long>(clock64() - task_t0);
+                S.diag[0] = S.ctr[W_TUPLES] - static_cast<unsigned long long>(tdiag[0]);  // decoded below
+                S.diag[1] = S.ctr[W_LEAVES] - static_cast<unsigned long long>(tdiag[1]);
+                S.diag[2] = S.ctr[W_NODES] - static_cast<unsigned long long>(tdiag[2]);
             }
             if (!ok) {
                 if (lane == 0) atomicOr(P.error_flag, 4);
@@ -1733,7 +1739,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                     r[4] = S.ctr[W_TUPLES] - S.diag[0];
                     r[5] = S.ctr[W_LEAVES] - S.diag[1];
                     r[6] = S.ctr[W_NODES] - S.diag[2];
-                    r[7] = S.ctr[W_VCMP] - S.diag[3];
+                    r[7] = kind == 0 ? 0ull : S.diag[3];  // cycles before the task's own search (claim + replays)
                 }
             }
             const int hb = kind == 0 ? C_HIST0 : (S.task.kind == 0 ? C_HIST_DON0 : C_HIST_DON1);

@@ -1,6 +1,10 @@
-for v in vhead base; do
-  if [ "$v" != base ]; then export PMS8G_LIB=$PWD/paper_1307_0571_b200/lib/$v/libpms8g.so; else unset PMS8G_LIB; fi
-  echo "== $v"; python scripts/profile_run.py 17 6 0 3 | grep -E "wall"; SHARD=0/8 python scripts/profile_run.py 17 6 0 3 | grep -E "wall"; SHARD=0/8 python scripts/profile_run.py 21 8 0 2 | grep -E "wall"
+for o in "" 1; do
+echo "no_order=$o"
+export PMS8G_NO_TASK_ORDER=$o; [ -z "$o" ] && unset PMS8G_NO_TASK_ORDER
+SHARD=0/8 python scripts/profile_run.py 17 6 0 2 | grep -E "wall|idle"
+python scripts/profile_run.py 17 6 0 2 | grep -E "wall|idle"
+SHARD=0/8 python scripts/profile_run.py 21 8 0 2 | grep -E "wall|idle"
+python scripts/profile_run.py 13 4 0 3 | grep -E "wall|idle"
 done
-unset PMS8G_LIB
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+unset PMS8G_NO_TASK_ORDER
+python -m pytest tests -m gpu -x -q 2>&1 | tail -1

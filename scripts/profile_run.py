@@ -43,7 +43,7 @@ if len(c) > 55:
     for i in range(nlog):
         r = c[137 + 8 * i:145 + 8 * i]
         print(f"  long task kind={r[0]} anchor={r[1]} idx={r[2]} cycles={r[3]:.3e} tuples={r[4]} leaves={r[5]} "
-              f"nodes={r[6]} vcmp={r[7]}")
+              f"nodes={r[6]} prologue_cycles={r[7]}")
     print(f"  idle warp-cycles {c[55]:.3e} busy(filter+pattern) {c[8] + c[9]:.3e}"
           + (f" of {tot:.3e} available: idle {c[55] / tot:.1%}" if tot else ""))
 print("  task cycles histogram (log2 bucket: count): " +
