@@ -11,6 +11,9 @@
  *                           re-runnable context: inputs stay in HBM between runs)
  *   pms8g_generate       <- generate_planted_instance include/pms8/instance.hpp:38
  *   pms8g_estimate_threshold <- estimate_threshold include/pms8/solver.hpp:61
+ *   pms8g_verify_motifs  <- naive_is_motif src/oracle.cpp:16-37 (`pms8 verify`, tools/pms8.cpp:193-256)
+ *   pms8g_brute_force    <- brute_force_solve src/oracle.cpp:65-75
+ *   pms8g_queue_*       <- the shared next-job counter of run_parallel src/parallel.cpp:54-60, across GPUs
  *   pms8g_merge_keys     <- canonical_motif_set  include/pms8/solver.hpp:22 (device sort+unique
  *                           of packed motif keys; used after the multi-GPU allgather)
  *
@@ -40,6 +43,8 @@ enum {
 
 /* Mirrors SolverConfig (include/pms8/solver.hpp:24-31) plus the device and
  * sharding knobs that replace ParallelOptions (include/pms8/parallel.hpp:22-28). */
+typedef struct pms8g_queue pms8g_queue; /* cross-GPU static task queue, see pms8g_queue_create */
+
 typedef struct pms8g_options {
     int threshold;         /* 0: GPU-tuned default; else 1..n (SolverConfig::threshold_override) */
     int sort_rows;         /* 1: branch on the smallest row (reference default) */
@@ -60,6 +65,10 @@ typedef struct pms8g_options {
                                 id seq*(m-l+1)+offset of an l-mer in that S1 l-mer's branching row);
                                 the result is the motif set under those branches only */
     int nbranches;
+    pms8g_queue* queue;    /* optional shared queue (multi-GPU dynamic pull over S1 l-mers, replacing the
+                              reference's shared atomic job counter src/parallel.cpp:54-60 across GPUs):
+                              every rank searches all S1 l-mers, claiming (S1 l-mer, depth-1 branch) tasks
+                              from one counter; exclusive with shard_count > 1 */
 } pms8g_options;
 
 /* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */
@@ -137,6 +146,32 @@ int pms8g_generate(int n, int m, int l, int d, int sigma, uint64_t seed, int exa
 /* Threshold model (src/solver.cpp:75-117) and the GPU-tuned default. */
 int pms8g_estimate_threshold(int n, int m, int l, int d, int sigma);
 int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma);
+
+/* Brute-force scanner (the reference's `pms8 verify` subcommand, tools/pms8.cpp:193-256, over
+ * naive_is_motif src/oracle.cpp:16-37), batched on the device: motifs = nmotifs*l codes in
+ * [0, sigma). pass[i] = 1 iff every sequence has a window within Hamming distance d;
+ * witness[i*n + r] = the first such offset in sequence r, -1 from the first sequence without
+ * one on (the reference stops there). device = -1: current device. */
+int pms8g_verify_motifs(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const uint8_t* motifs,
+                        int64_t nmotifs, int32_t* witness, uint8_t* pass, int device, char* err, size_t errlen);
+/* Exhaustive solver over Sigma^l (brute_force_solve src/oracle.cpp:65-75): every word, in
+ * code order, checked against every sequence; sorted motif set out. sigma^l > guard ->
+ * PMS8G_ERR_INVALID (check_guard src/oracle.cpp:41-46; the reference's default guard is 10^6,
+ * include/pms8/oracle.hpp:28-29). Independent of the PMS8 tree: an exactness check. */
+int pms8g_brute_force(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, int64_t guard,
+                      int device, pms8g_result* out, char* err, size_t errlen);
+
+/* Cross-GPU static task queue: one 64-bit claim counter in the HBM of the creating rank's
+ * device, mapped into the other ranks' devices over NVLink/NVSwitch with CUDA IPC. Rank 0
+ * creates it and passes `handle` (PMS8G_QUEUE_HANDLE_BYTES) to the others, which open it on
+ * their own device; each rank then sets pms8g_options.queue. The counter is epoch-tagged, so
+ * consecutive runs need no reset, as long as every rank issues the same sequence of runs
+ * (the per-run motif allgather keeps them in step). Replaces the reference's
+ * std::atomic<int> next-job counter (src/parallel.cpp:54-60) at node scale. */
+#define PMS8G_QUEUE_HANDLE_BYTES 64
+int pms8g_queue_create(int device, pms8g_queue** out, uint8_t* handle, char* err, size_t errlen);
+int pms8g_queue_open(const uint8_t* handle, int device, pms8g_queue** out, char* err, size_t errlen);
+void pms8g_queue_destroy(pms8g_queue* q);
 
 /* Integer-pipe peak microbenchmark: LOP3/IADD3-class ops per second over all
  * SMs of `device` (measured, used as the roofline denominator), and the SM

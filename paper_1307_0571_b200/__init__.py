@@ -11,6 +11,8 @@ Host-side mirror of the reference's solver interface (/root/reference/proj):
     split_subproblems, resolve_worker_count        include/pms8/parallel.hpp:16-33
     generate_planted_instance                      include/pms8/instance.hpp:23-38
     estimate_threshold                             include/pms8/solver.hpp:61
+    naive_is_motif, verify_motifs, brute_force_solve  include/pms8/oracle.hpp:14-29 (the
+                                   brute-force scanner behind `pms8 verify`, run on the GPU)
 
 Every search call goes through the C ABI of lib/libpms8g.so (include/pms8g.h)
 to the CUDA kernels; there is no CPU path. Errors map to the reference's
@@ -33,7 +35,7 @@ __all__ = [
     "MotifSet", "solve", "run_parallel", "split_subproblems", "resolve_worker_count", "generate_planted_instance",
     "PlantedInstanceSpec", "PlantedInstance", "MutationMode", "estimate_threshold", "gpu_threshold",
     "InvalidArgument", "SolverRuntimeError", "SolverLogicError", "DeviceError", "ExtensionMissing", "Context",
-    "canonical_motif_set",
+    "canonical_motif_set", "naive_is_motif", "verify_motifs", "brute_force_solve",
 ]
 
 MotifSet = List[str]
@@ -190,6 +192,8 @@ class ParallelOptions:
     blocks_per_sm: int = 0
     exact_tree: bool = False  # True: same search tree as the reference (every row filtered at every push)
     branches: Optional[Sequence] = None  # explicit depth-1 branches [(s1_offset, seq, offset), ...]
+    queue: Optional[object] = None  # parallel.SharedQueue: cross-GPU dynamic pull (exclusive with shard_count > 1)
+    split: str = "queue"  # run_parallel under torch.distributed: "queue" (shared cross-GPU queue) or "static"
 
 
 @dataclasses.dataclass
@@ -269,6 +273,8 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions], win
     o.warps_per_block = int(par.warps_per_block)
     o.blocks_per_sm = int(par.blocks_per_sm)
     o.exact_tree = 1 if par.exact_tree else 0
+    if par.queue is not None:
+        o.queue = par.queue.ptr
     keep = None
     if par.branches is not None:
         # (S1 offset, seq, offset) -> (S1 offset, l-mer id = seq * (m-l+1) + offset)
@@ -331,12 +337,79 @@ def run_parallel(problem: Problem, config: Optional[SolverConfig] = None,
     options = options or ParallelOptions()
     from . import parallel as _par
     if _par.distributed_world() > 1 and options.shard_count == 1:
-        return _par.run_sharded(problem, config, options, report)
+        return _par.run_sharded(problem, config, options, report, split=options.split)
     codes = _validated(problem)
     out = _solve_codes(codes, problem.motif_length, problem.max_mismatches, problem.alphabet, config, options, report)
     if report is not None:
         report.workers = max(1, options.workers or 1)
     return out
+
+
+def verify_motifs(problem: Problem, motifs: Sequence[str], device: int = -1):
+    """Brute-force scan of candidate motifs on the GPU (`pms8 verify`,
+    tools/pms8.cpp:193-256): one (passed, witness offsets) pair per motif,
+    with naive_is_motif's semantics (src/oracle.cpp:16-37) — the witnesses
+    are the first window within d in each sequence, up to the first sequence
+    without one (an empty list for a failing motif stops there too)."""
+    codes = _validated(problem)
+    l, n = problem.motif_length, problem.n()
+    for mt in motifs:
+        if len(mt) != l:
+            raise InvalidArgument(f"motif {mt} has length {len(mt)}, expected l={l}")
+        for ch in mt:
+            if not problem.alphabet.contains(ch):
+                raise InvalidArgument(f"motif {mt} contains symbol '{ch}' outside alphabet {problem.alphabet.name()}")
+    if not motifs:
+        return []
+    mc = problem.alphabet.encode(list(motifs))
+    wit = np.zeros((len(motifs), n), np.int32)
+    ok = np.zeros(len(motifs), np.uint8)
+    err = ctypes.create_string_buffer(512)
+    rc = _capi.lib().pms8g_verify_motifs(codes.ctypes.data, n, problem.m(), l, problem.max_mismatches,
+                                         problem.alphabet.symbols.encode(), mc.ctypes.data, len(motifs),
+                                         wit.ctypes.data, ok.ctypes.data, device, err, len(err))
+    if rc != 0:
+        _raise(rc, err)
+    out = []
+    for i in range(len(motifs)):
+        offs = [int(x) for x in wit[i]]
+        if ok[i]:
+            out.append((True, offs))
+        else:
+            out.append((False, offs[:offs.index(-1)]))
+    return out
+
+
+def naive_is_motif(problem: Problem, motif: str, witness_offsets: Optional[list] = None) -> bool:
+    """naive_is_motif (src/oracle.cpp:16-37) on the GPU scanner."""
+    ok, offs = verify_motifs(problem, [motif])[0]
+    if witness_offsets is not None:
+        witness_offsets[:] = offs
+    return ok
+
+
+def brute_force_solve(problem: Problem, enumeration_guard: int = 1000000, report: Optional[RunReport] = None,
+                      device: int = -1) -> MotifSet:
+    """Exhaustive Sigma^l solver on the GPU (brute_force_solve,
+    src/oracle.cpp:65-75; sigma^l > guard raises InvalidArgument)."""
+    codes = _validated(problem)
+    res = _capi.Result()
+    err = ctypes.create_string_buffer(512)
+    L = _capi.lib()
+    l = problem.motif_length
+    rc = L.pms8g_brute_force(codes.ctypes.data, problem.n(), problem.m(), l, problem.max_mismatches,
+                             problem.alphabet.symbols.encode(), int(enumeration_guard), device, ctypes.byref(res),
+                             err, len(err))
+    if rc != 0:
+        _raise(rc, err)
+    try:
+        raw = ctypes.string_at(res.motifs, res.count * res.l).decode() if res.count else ""
+        motifs = [raw[i * l:(i + 1) * l] for i in range(res.count)]
+        if report is not None:
+            report.fill(res.report, problem.alphabet.name())
+    finally:
+        L.pms8g_result_free(ctypes.byref(res))
+    return motifs
 
 
 def split_subproblems(problem: Problem):

@@ -34,6 +34,7 @@ class Options(ctypes.Structure):
         ("exact_tree", ctypes.c_int),
         ("branches", ctypes.POINTER(ctypes.c_int32)),
         ("nbranches", ctypes.c_int),
+        ("queue", ctypes.c_void_p),
     ]
 
 
@@ -69,8 +70,10 @@ EXPORTS = [
     "pms8g_ctx_run", "pms8g_ctx_keys", "pms8g_ctx_result", "pms8g_ctx_stream", "pms8g_ctx_kernel_ms",
     "pms8g_ctx_counters",
     "pms8g_ctx_destroy", "pms8g_merge_keys", "pms8g_decode_keys", "pms8g_generate", "pms8g_estimate_threshold",
-    "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version",
+    "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version", "pms8g_verify_motifs", "pms8g_brute_force",
+    "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy",
 ]
+QUEUE_HANDLE_BYTES = 64
 
 _lib = None
 
@@ -125,6 +128,18 @@ def lib():
     L.pms8g_int_peak.argtypes = [c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                  c_char_p, c_sz]
     L.pms8g_int_peak.restype = c_int
+    L.pms8g_verify_motifs.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_char_p, c_vp, c_i64, c_vp, c_vp, c_int,
+                                      c_char_p, c_sz]
+    L.pms8g_verify_motifs.restype = c_int
+    L.pms8g_brute_force.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_char_p, c_i64, c_int,
+                                    ctypes.POINTER(Result), c_char_p, c_sz]
+    L.pms8g_brute_force.restype = c_int
+    L.pms8g_queue_create.argtypes = [c_int, ctypes.POINTER(c_vp), c_vp, c_char_p, c_sz]
+    L.pms8g_queue_create.restype = c_int
+    L.pms8g_queue_open.argtypes = [c_vp, c_int, ctypes.POINTER(c_vp), c_char_p, c_sz]
+    L.pms8g_queue_open.restype = c_int
+    L.pms8g_queue_destroy.argtypes = [c_vp]
+    L.pms8g_queue_destroy.restype = None
     L.pms8g_version.argtypes = []
     L.pms8g_version.restype = c_char_p
     _lib = L

@@ -8,6 +8,8 @@
 //   pms8::solve            include/pms8/solver.hpp:180
 //   pms8::run_parallel     include/pms8/parallel.hpp:37-38
 //   pms8::read_sequences   include/pms8/io.hpp:21 (FASTA/plain, metadata)
+//   pms8::naive_is_motif   include/pms8/oracle.hpp:14-22 (batched: verify_motifs)
+//   pms8::brute_force_solve include/pms8/oracle.hpp:27-29
 //
 // Errors are rethrown as the reference's exception classes.
 #pragma once
@@ -80,6 +82,17 @@ struct SequenceFile {
     std::map<std::string, std::string> metadata;
 };
 SequenceFile read_sequences(const std::string& path);
+SequenceFile read_plain(const std::string& path);  // src/io.cpp:99
+
+// Brute-force scanner on the GPU (pms8g_verify_motifs / pms8g_brute_force).
+struct MotifCheck {
+    bool pass = false;
+    std::vector<int> witness_offsets;  // first window within d per sequence, up to the first miss
+};
+std::vector<MotifCheck> verify_motifs(const Problem& problem, const std::vector<std::string>& motifs,
+                                      int device = -1);
+bool naive_is_motif(const Problem& problem, const std::string& motif, std::vector<int>* witness_offsets = nullptr);
+MotifSet brute_force_solve(const Problem& problem, int64_t enumeration_guard = 1000000, int device = -1);
 void write_fasta(const std::string& path, const std::vector<std::string>& names,
                  const std::vector<std::string>& sequences,
                  const std::vector<std::pair<std::string, std::string>>& metadata);

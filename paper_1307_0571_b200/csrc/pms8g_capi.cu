@@ -69,6 +69,13 @@ unsigned __int128 nsize(int l, int d, int sigma) {
 
 }  // namespace
 
+struct pms8g_queue {
+    void* dptr = nullptr;       // the shared counter, mapped on this rank's device
+    int device = 0;
+    int owner = 0;              // 1: allocated here (cudaFree), 0: IPC-opened (cudaIpcCloseMemHandle)
+    unsigned long long epoch = 0;  // runs issued through this queue by this rank
+};
+
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
     std::string alphabet;
@@ -210,7 +217,62 @@ void pms8g_default_options(pms8g_options* o) {
     o->max_motifs = -1;
 }
 
-const char* pms8g_version(void) { return "pms8g 0.1 (sm_100a)"; }
+const char* pms8g_version(void) { return "pms8g 0.2 (sm_100a)"; }
+
+int pms8g_queue_create(int device, pms8g_queue** out, uint8_t* handle, char* err, size_t errlen) {
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "no CUDA device available (%s); the GPU path has no CPU fallback",
+                    cudaGetErrorString(ce));
+    if (device >= 0) CU(cudaSetDevice(device));
+    auto* q = new pms8g_queue();
+    CU(cudaGetDevice(&q->device));
+    q->owner = 1;
+    if (cudaMalloc(&q->dptr, 256) != cudaSuccess) {
+        delete q;
+        return fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate the shared queue");
+    }
+    CU(cudaMemset(q->dptr, 0, 256));
+    CU(cudaDeviceSynchronize());
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, q->dptr));
+    static_assert(sizeof(cudaIpcMemHandle_t) == PMS8G_QUEUE_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof h);
+    *out = q;
+    return PMS8G_OK;
+}
+
+int pms8g_queue_open(const uint8_t* handle, int device, pms8g_queue** out, char* err, size_t errlen) {
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "no CUDA device available (%s); the GPU path has no CPU fallback",
+                    cudaGetErrorString(ce));
+    if (device >= 0) CU(cudaSetDevice(device));
+    auto* q = new pms8g_queue();
+    CU(cudaGetDevice(&q->device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    ce = cudaIpcOpenMemHandle(&q->dptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (ce != cudaSuccess) {
+        delete q;
+        return fail(err, errlen, PMS8G_ERR_CUDA, "cannot map the shared queue on device %d (%s)", device,
+                    cudaGetErrorString(ce));
+    }
+    *out = q;
+    return PMS8G_OK;
+}
+
+void pms8g_queue_destroy(pms8g_queue* q) {
+    if (!q) return;
+    cudaSetDevice(q->device);
+    if (q->owner) cudaFree(q->dptr);
+    else cudaIpcCloseMemHandle(q->dptr);
+    delete q;
+}
 
 int pms8g_estimate_threshold(int n, int m, int l, int d, int sigma) {
     // threshold_curve + estimate_threshold, src/solver.cpp:75-117
@@ -326,6 +388,8 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     int t = 0;
     if ((rc = resolve_threshold(n, m, l, d, sigma, opt.threshold, err, errlen, &t))) return rc;
     if (opt.shard_count < 1) opt.shard_count = 1;
+    if (opt.queue && opt.shard_count > 1)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "a shared queue replaces sharding: shard_count must be 1");
     if (opt.shard_rank < 0 || opt.shard_rank >= opt.shard_count)
         return fail(err, errlen, PMS8G_ERR_INVALID, "shard rank %d outside [0, %d)", opt.shard_rank, opt.shard_count);
 
@@ -625,7 +689,7 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
            c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
            (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && o.branches == nullptr &&
            c->opt.warps_per_block == o.warps_per_block &&
-           c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree;
+           c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree && c->opt.queue == o.queue;
 }
 }  // namespace
 
@@ -695,6 +759,191 @@ int pms8g_int_peak(int device, double* ops_per_second, double* popc_per_second, 
     cudaFree(sink);
     if (ops_per_second) *ops_per_second = res[0];
     if (popc_per_second) *popc_per_second = res[1];
+    return PMS8G_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Problem::validate (src/problem.cpp:7-28) plus the scanner's device limits
+// (2 bit planes: at most 4 symbols, l <= 64); codes checked against sigma.
+int validate_scan(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, char* err, size_t errlen,
+                  int* sigma) {
+    if (n < 1) return fail(err, errlen, PMS8G_ERR_INVALID, "no input sequences");
+    if (l < 1) return fail(err, errlen, PMS8G_ERR_INVALID, "motif length must be >= 1");
+    if (l > m) return fail(err, errlen, PMS8G_ERR_INVALID, "motif length %d exceeds sequence length %d", l, m);
+    if (d < 0 || d > l) return fail(err, errlen, PMS8G_ERR_INVALID, "mismatch budget must be in [0, l], got %d", d);
+    const int s = alphabet ? static_cast<int>(std::strlen(alphabet)) : 4;
+    if (s < 2) return fail(err, errlen, PMS8G_ERR_INVALID, "alphabet needs at least 2 symbols");
+    if (s > 4)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 4 symbols, got %d", s);
+    if (l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
+    const size_t bytes = static_cast<size_t>(n) * m;
+    for (size_t i = 0; i < bytes; ++i)
+        if (codes[i] >= s)
+            return fail(err, errlen, PMS8G_ERR_INVALID, "sequence %zu, position %zu: code %d not in alphabet %s",
+                        i / m, i % m, codes[i], alphabet ? alphabet : "ACGT");
+    *sigma = s;
+    return PMS8G_OK;
+}
+
+// Device buffers of one scanner call (freed on every exit path).
+struct ScanBufs {
+    uint8_t* codes = nullptr;
+    void* table = nullptr;
+    int* flag = nullptr;
+    void* a = nullptr;
+    void* b = nullptr;
+    void* c = nullptr;
+    cudaStream_t stream = nullptr;
+    ~ScanBufs() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : {static_cast<void*>(codes), table, static_cast<void*>(flag), a, b, c})
+            if (p) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+// H2D codes + K1 encode into a fresh l-mer table.
+int scan_setup(ScanBufs& B, const uint8_t* codes, int n, int m, int l, int device, int* W, int* w, char* err,
+               size_t errlen) {
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "no CUDA device available (%s); the GPU path has no CPU fallback",
+                    cudaGetErrorString(ce));
+    if (device >= ndev)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "device %d not present (%d devices)", device, ndev);
+    if (device >= 0) CU(cudaSetDevice(device));
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100-class; kernels are sm_100a only",
+                    dev, prop.name, prop.major, prop.minor);
+    CU(cudaStreamCreateWithFlags(&B.stream, cudaStreamNonBlocking));
+    *W = l <= 32 ? 1 : 2;
+    *w = m - l + 1;
+    const size_t bytes = static_cast<size_t>(n) * m;
+    CU(cudaMalloc(&B.codes, bytes));
+    CU(cudaMalloc(&B.table, static_cast<size_t>(n) * *w * lmer_bytes(*W)));
+    CU(cudaMalloc(&B.flag, sizeof(int)));
+    CU(cudaMemsetAsync(B.flag, 0, sizeof(int), B.stream));
+    CU(cudaMemcpyAsync(B.codes, codes, bytes, cudaMemcpyHostToDevice, B.stream));
+    CU(launch_encode(*W, B.codes, n, m, l, *w, B.table, B.flag, B.stream));
+    return PMS8G_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pms8g_verify_motifs(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const uint8_t* motifs,
+                        int64_t nmotifs, int32_t* witness, uint8_t* pass, int device, char* err, size_t errlen) {
+    int sigma = 0;
+    int rc = validate_scan(codes, n, m, l, d, alphabet, err, errlen, &sigma);
+    if (rc) return rc;
+    if (nmotifs < 0) return fail(err, errlen, PMS8G_ERR_INVALID, "negative motif count");
+    for (int64_t i = 0; i < nmotifs * l; ++i)
+        if (motifs[i] >= sigma)
+            return fail(err, errlen, PMS8G_ERR_INVALID, "motif %lld contains a code outside the alphabet",
+                        static_cast<long long>(i / l));
+    if (nmotifs == 0) return PMS8G_OK;
+    ScanBufs B;
+    int W = 1, w = 0;
+    if ((rc = scan_setup(B, codes, n, m, l, device, &W, &w, err, errlen))) return rc;
+    CU(cudaMalloc(&B.a, static_cast<size_t>(nmotifs) * l));
+    CU(cudaMalloc(&B.b, static_cast<size_t>(nmotifs) * n * sizeof(int32_t)));
+    CU(cudaMalloc(&B.c, static_cast<size_t>(nmotifs)));
+    CU(cudaMemcpyAsync(B.a, motifs, static_cast<size_t>(nmotifs) * l, cudaMemcpyHostToDevice, B.stream));
+    CU(launch_witness(W, B.table, n, w, l, d, sigma, static_cast<const uint8_t*>(B.a), nmotifs,
+                      static_cast<int32_t*>(B.b), static_cast<uint8_t*>(B.c), B.stream));
+    CU(cudaMemcpyAsync(witness, B.b, static_cast<size_t>(nmotifs) * n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       B.stream));
+    CU(cudaMemcpyAsync(pass, B.c, static_cast<size_t>(nmotifs), cudaMemcpyDeviceToHost, B.stream));
+    CU(cudaStreamSynchronize(B.stream));
+    return PMS8G_OK;
+}
+
+int pms8g_brute_force(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, int64_t guard,
+                      int device, pms8g_result* out, char* err, size_t errlen) {
+    const double t0 = now_s();
+    std::memset(out, 0, sizeof *out);
+    int sigma = 0;
+    int rc = validate_scan(codes, n, m, l, d, alphabet, err, errlen, &sigma);
+    if (rc) return rc;
+    // check_guard, src/oracle.cpp:41-46
+    const long double space = std::pow(static_cast<long double>(sigma), l);
+    if (space > static_cast<long double>(guard))
+        return fail(err, errlen, PMS8G_ERR_INVALID, "enumeration space %d^%d exceeds guard %lld", sigma, l,
+                    static_cast<long long>(guard));
+    unsigned long long total = 1;
+    for (int p = 0; p < l; ++p) total *= static_cast<unsigned long long>(sigma);
+    ScanBufs B;
+    int W = 1, w = 0;
+    if ((rc = scan_setup(B, codes, n, m, l, device, &W, &w, err, errlen))) return rc;
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    long long cap = static_cast<long long>(std::min<unsigned long long>(total, 1ull << 20));
+    unsigned long long found = 0;
+    float ms = 0.f;
+    for (int pass = 0; pass < 2; ++pass) {
+        if (B.a) cudaFree(B.a);
+        B.a = nullptr;
+        CU(cudaMalloc(&B.a, 16 * static_cast<size_t>(std::max(1ll, cap))));
+        if (!B.b) CU(cudaMalloc(&B.b, sizeof(unsigned long long)));
+        CU(cudaMemsetAsync(B.b, 0, sizeof(unsigned long long), B.stream));
+        CU(cudaEventRecord(e0, B.stream));
+        CU(launch_sweep(W, B.table, n, w, l, d, sigma, total, static_cast<unsigned long long*>(B.a),
+                        static_cast<unsigned long long*>(B.b), cap, sms, B.stream));
+        CU(cudaEventRecord(e1, B.stream));
+        CU(cudaMemcpyAsync(&found, B.b, sizeof found, cudaMemcpyDeviceToHost, B.stream));
+        CU(cudaStreamSynchronize(B.stream));
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        if (static_cast<long long>(found) <= cap) break;
+        cap = static_cast<long long>(found);  // second pass with room for every motif
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const long long cnt = static_cast<long long>(found);
+    std::vector<uint64_t> keys(2 * static_cast<size_t>(cnt));
+    if (cnt > 0) {
+        CU(cudaMalloc(&B.c, 16 * static_cast<size_t>(cnt)));
+        int64_t uniq = 0;
+        if ((rc = pms8g_merge_keys(static_cast<const uint64_t*>(B.a), cnt, static_cast<uint64_t*>(B.c), &uniq,
+                                   B.stream, err, errlen)))
+            return rc;
+        CU(cudaMemcpyAsync(keys.data(), B.c, 16 * static_cast<size_t>(uniq), cudaMemcpyDeviceToHost, B.stream));
+        CU(cudaStreamSynchronize(B.stream));
+        keys.resize(2 * static_cast<size_t>(uniq));
+    }
+    const long long uniq = static_cast<long long>(keys.size() / 2);
+    out->l = l;
+    out->count = uniq;
+    out->motifs = static_cast<char*>(std::malloc(static_cast<size_t>(uniq) * l + 1));
+    if (!out->motifs) return fail(err, errlen, PMS8G_ERR_RUNTIME, "cannot allocate motif buffer");
+    pms8g_decode_keys(keys.data(), uniq, l, alphabet ? alphabet : "ACGT", out->motifs);
+    out->motifs[static_cast<size_t>(uniq) * l] = 0;
+    pms8g_report& R = out->report;
+    R.n = n;
+    R.m = m;
+    R.l = l;
+    R.d = d;
+    R.sigma = sigma;
+    R.gpus = 1;
+    R.motif_count = uniq;
+    R.motifs_emitted = cnt;
+    R.neighbors_visited = static_cast<int64_t>(total);
+    R.device_seconds = ms * 1e-3;
+    R.pattern_seconds = ms * 1e-3;
+    R.wall_seconds = now_s() - t0;
     return PMS8G_OK;
 }
 
@@ -776,6 +1025,12 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.key_cap = c->key_cap;
         P.counters = c->d_counters;
         P.error_flag = c->d_err;
+        P.gqueue = nullptr;
+        P.gepoch = 0;
+        if (c->opt.queue) {
+            P.gqueue = static_cast<unsigned long long*>(c->opt.queue->dptr);
+            P.gepoch = ++c->opt.queue->epoch;
+        }
         const char* tl_path = std::getenv("PMS8G_TIMELINE");  // diagnostics: task timeline dump
         unsigned long long* d_tl = nullptr;
         if (tl_path) {

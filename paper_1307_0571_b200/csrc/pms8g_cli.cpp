@@ -3,6 +3,7 @@
 //   pms8g solve <input> [-l L] [-d D] [--alphabet A] [--workers N] [--threshold T]
 //               [--max-motifs K] [--format text|json] [--prune none|pairs|full]
 //               [--no-sort-rows] [--no-pair-matrix] [--reverify] [--device N]
+//   pms8g verify <input> -M MOTIFS [-l L] [-d D] [--alphabet A] [--device N]
 //   pms8g generate -l L -d D [-n N] [-m M] [--alphabet A] [--seed S]
 //               [--mutation atmost|exact] [-o FILE]
 //
@@ -147,6 +148,92 @@ int cmd_solve(const std::vector<std::string>& args, const std::string& command) 
     return motifs.empty() ? 1 : 0;
 }
 
+// cmd_verify (tools/pms8.cpp:193-256): one line per candidate, `motif\tPASS\t
+// offsets` or `motif\tFAIL`; exit 0 if all pass, 1 otherwise, 2 on bad input.
+// The scan runs on the GPU (pms8g_verify_motifs).
+int cmd_verify(const std::vector<std::string>& args) {
+    std::string input, motifs_path, alphabet;
+    std::optional<int> l, d;
+    int device = -1;
+    for (size_t i = 0; i < args.size(); ++i) {
+        const std::string& a = args[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= args.size()) throw Usage(a + " needs a value");
+            return args[++i];
+        };
+        if (a == "-l") l = to_int(a, val());
+        else if (a == "-d") d = to_int(a, val());
+        else if (a == "-M" || a == "--motifs") motifs_path = val();
+        else if (a == "--alphabet") alphabet = val();
+        else if (a == "--device") device = to_int(a, val());
+        else if (!a.empty() && a[0] == '-') throw Usage("unknown option " + a);
+        else if (input.empty()) input = a;
+        else throw Usage("unexpected argument " + a);
+    }
+    if (input.empty()) throw Usage("verify: input file required");
+    if (motifs_path.empty()) throw Usage("verify: --motifs is required");
+    const pms8g::SequenceFile file = pms8g::read_sequences(input);
+    auto meta_int = [&](const char* key) -> std::optional<int> {
+        auto it = file.metadata.find(key);
+        if (it == file.metadata.end()) return std::nullopt;
+        return std::stoi(it->second);
+    };
+    if (!l) l = meta_int("l");
+    if (!d) d = meta_int("d");
+    if (!l || !d) {
+        std::cerr << "error: -l and -d are required (no l/d metadata in " << input << ")\n";
+        return 2;
+    }
+    if (alphabet.empty()) {
+        auto it = file.metadata.find("alphabet");
+        alphabet = it != file.metadata.end() ? it->second : "dna";
+    }
+    pms8g::Problem problem;
+    problem.sequences = file.sequences;
+    problem.motif_length = *l;
+    problem.max_mismatches = *d;
+    problem.alphabet = pms8g::alphabet_symbols(alphabet);
+    problem.alphabet_name = alphabet;
+    problem.validate();
+    const pms8g::SequenceFile motif_file = pms8g::read_plain(motifs_path);
+    // the reference reports the motifs before the first malformed one, then
+    // fails on it (tools/pms8.cpp:219-253): scan that prefix in one batch
+    std::vector<std::string> good;
+    std::string bad_msg;
+    for (const std::string& motif : motif_file.sequences) {
+        if (static_cast<int>(motif.size()) != *l) {
+            bad_msg = "motif " + motif + " has length " + std::to_string(motif.size()) + ", expected l=" +
+                      std::to_string(*l);
+            break;
+        }
+        for (char c : motif)
+            if (bad_msg.empty() && problem.alphabet.find(c) == std::string::npos)
+                bad_msg = "motif " + motif + " contains symbol '" + std::string(1, c) + "' outside alphabet " +
+                          alphabet;
+        if (!bad_msg.empty()) break;
+        good.push_back(motif);
+    }
+    const std::vector<pms8g::MotifCheck> checks = pms8g::verify_motifs(problem, good, device);
+    bool all_pass = true;
+    for (size_t i = 0; i < checks.size(); ++i) {
+        const std::string& motif = good[i];
+        if (checks[i].pass) {
+            std::cout << motif << "\tPASS\t";
+            for (size_t k = 0; k < checks[i].witness_offsets.size(); ++k)
+                std::cout << (k ? "," : "") << checks[i].witness_offsets[k];
+            std::cout << "\n";
+        } else {
+            std::cout << motif << "\tFAIL\n";
+            all_pass = false;
+        }
+    }
+    if (!bad_msg.empty()) {
+        std::cerr << "error: " << bad_msg << "\n";
+        return 2;
+    }
+    return all_pass ? 0 : 1;
+}
+
 int cmd_generate(const std::vector<std::string>& args) {
     int l = -1, d = -1, n = 20, m = 600;
     std::string alphabet = "dna", mutation = "atmost", output = "instance.fa";
@@ -203,11 +290,12 @@ int main(int argc, char** argv) {
     std::string command;
     for (int i = 0; i < argc; ++i) command += (i ? " " : "") + std::string(argv[i]);
     try {
-        if (args.empty()) throw Usage("a subcommand is required: solve | generate");
+        if (args.empty()) throw Usage("a subcommand is required: solve | verify | generate");
         const std::string sub = args[0];
         args.erase(args.begin());
         if (sub == "solve") return cmd_solve(args, command);
         if (sub == "generate") return cmd_generate(args);
+        if (sub == "verify") return cmd_verify(args);
         throw Usage("unknown subcommand " + sub);
     } catch (const Usage& e) {
         std::cerr << "usage error: " << e.what() << "\n";

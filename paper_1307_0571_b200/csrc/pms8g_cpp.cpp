@@ -196,6 +196,68 @@ MotifSet solve(const Problem& problem, const SolverConfig& config, RunReport* re
     return run_parallel(problem, config, GpuOptions{}, report);
 }
 
+SequenceFile read_plain(const std::string& path) { return parse_plain(slurp(path)); }
+
+namespace {
+std::vector<uint8_t> encode_codes(const std::vector<std::string>& seqs, const std::string& alphabet) {
+    std::vector<uint8_t> codes;
+    for (const auto& s : seqs)
+        for (char ch : s) codes.push_back(static_cast<uint8_t>(alphabet.find(ch)));
+    return codes;
+}
+}  // namespace
+
+std::vector<MotifCheck> verify_motifs(const Problem& problem, const std::vector<std::string>& motifs, int device) {
+    problem.validate();
+    const int n = problem.n(), m = problem.m(), l = problem.motif_length;
+    for (const auto& mt : motifs) {
+        if (static_cast<int>(mt.size()) != l)
+            throw std::invalid_argument("motif " + mt + " has length " + std::to_string(mt.size()) +
+                                        ", expected l=" + std::to_string(l));
+        for (char ch : mt)
+            if (problem.alphabet.find(ch) == std::string::npos)
+                throw std::invalid_argument("motif " + mt + " contains symbol '" + ch + "' outside alphabet " +
+                                            problem.alphabet_name);
+    }
+    std::vector<MotifCheck> out(motifs.size());
+    if (motifs.empty()) return out;
+    const std::vector<uint8_t> codes = encode_codes(problem.sequences, problem.alphabet);
+    const std::vector<uint8_t> mc = encode_codes(motifs, problem.alphabet);
+    std::vector<int32_t> wit(motifs.size() * n);
+    std::vector<uint8_t> pass(motifs.size());
+    char err[512] = {0};
+    const int rc = pms8g_verify_motifs(codes.data(), n, m, l, problem.max_mismatches, problem.alphabet.c_str(),
+                                       mc.data(), static_cast<int64_t>(motifs.size()), wit.data(), pass.data(),
+                                       device, err, sizeof err);
+    if (rc != PMS8G_OK) rethrow(rc, err);
+    for (size_t i = 0; i < motifs.size(); ++i) {
+        out[i].pass = pass[i] != 0;
+        for (int r = 0; r < n && wit[i * n + r] >= 0; ++r) out[i].witness_offsets.push_back(wit[i * n + r]);
+    }
+    return out;
+}
+
+bool naive_is_motif(const Problem& problem, const std::string& motif, std::vector<int>* witness_offsets) {
+    const MotifCheck c = verify_motifs(problem, {motif})[0];
+    if (witness_offsets) *witness_offsets = c.witness_offsets;
+    return c.pass;
+}
+
+MotifSet brute_force_solve(const Problem& problem, int64_t enumeration_guard, int device) {
+    problem.validate();
+    const std::vector<uint8_t> codes = encode_codes(problem.sequences, problem.alphabet);
+    pms8g_result res;
+    char err[512] = {0};
+    const int rc = pms8g_brute_force(codes.data(), problem.n(), problem.m(), problem.motif_length,
+                                     problem.max_mismatches, problem.alphabet.c_str(), enumeration_guard, device,
+                                     &res, err, sizeof err);
+    if (rc != PMS8G_OK) rethrow(rc, err);
+    MotifSet motifs;
+    for (int64_t i = 0; i < res.count; ++i) motifs.emplace_back(res.motifs + i * res.l, res.l);
+    pms8g_result_free(&res);
+    return motifs;
+}
+
 SequenceFile read_sequences(const std::string& path) {
     // format sniff, src/io.cpp:101-111
     const std::string text = slurp(path);

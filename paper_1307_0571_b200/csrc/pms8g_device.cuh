@@ -56,6 +56,7 @@ enum Ctr {
     C_LOGN = C_HIST_DON1 + 40,       // diagnostics: number of long tasks logged
     C_LOG0,                          // 32 records x 8 words: kind, anchor, idx, cycles, tuples, leaves, nodes, vcmp
     C_TLN = C_LOG0 + 256,            // diagnostics: timeline records written
+    C_STATIC,                        // static tasks claimed by this device
     C_NCTR
 };
 
@@ -131,6 +132,14 @@ struct SearchParams {
     long long key_cap;
     unsigned long long* counters;
     int* error_flag;
+    // cross-GPU static queue (pms8g_queue): when set, static
+    // tasks are claimed from this counter in another (or this) device's HBM,
+    // shared by every rank over NVLink: value = epoch << 40 | next task
+    unsigned long long* gqueue;
+    unsigned long long gepoch;
 };
+
+constexpr int GQ_SHIFT = 40;
+constexpr unsigned long long GQ_MASK = (1ull << GQ_SHIFT) - 1ull;
 
 }  // namespace pms8g

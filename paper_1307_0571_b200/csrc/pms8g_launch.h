@@ -29,6 +29,11 @@ cudaError_t set_search_smem(int W, int t, size_t bytes);
 cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s);
 cudaError_t launch_reverify(int W, const void* table, int n, int w, int l, int d, const unsigned long long* keys,
                             long long count, int* fail, cudaStream_t s);
+cudaError_t launch_witness(int W, const void* table, int n, int w, int l, int d, int sigma, const uint8_t* motifs,
+                           long long nmotifs, int32_t* witness, uint8_t* pass, cudaStream_t s);
+cudaError_t launch_sweep(int W, const void* table, int n, int w, int l, int d, int sigma, unsigned long long total,
+                         unsigned long long* keys, unsigned long long* count, long long cap, int sms,
+                         cudaStream_t s);
 cudaError_t launch_intpeak(int which, int blocks, int threads, int iters, uint32_t* sink, cudaStream_t s);
 
 }  // namespace pms8g

@@ -108,6 +108,51 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 __device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
     return *reinterpret_cast<const volatile unsigned int*>(p);
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ---------------------------------------------------------------- static tasks
+// Static tasks come from the device-local counter, or (multi-GPU) from the
+// shared queue counter every rank claims from over NVLink. The shared counter
+// carries an epoch (one per run, advanced in the same order on every rank):
+// a run that finds an older epoch opens its own at task 0, one that finds a
+// newer epoch knows every task of its run was claimed already (a rank only
+// moves on once the previous run's counter was exhausted), so the counter
+// never needs a reset between runs.
+__device__ __forceinline__ bool statics_left(const SearchParams& P, unsigned long long nstatic) {
+    if (!P.gqueue) return ld_volatile(&P.qs->static_next) < nstatic;
+    const unsigned long long v = ld_relaxed_sys(P.gqueue);
+    const unsigned long long ep = v >> GQ_SHIFT;
+    return ep < P.gepoch || (ep == P.gepoch && (v & GQ_MASK) < nstatic);
+}
+
+__device__ __forceinline__ bool claim_static(const SearchParams& P, unsigned long long nstatic,
+                                             unsigned long long& idx) {
+    if (!P.gqueue) {
+        idx = atomicAdd(&P.qs->static_next, 1ull);
+        return idx < nstatic;
+    }
+    unsigned long long v = ld_relaxed_sys(P.gqueue);
+    for (;;) {
+        const unsigned long long ep = v >> GQ_SHIFT, cnt = v & GQ_MASK;
+        unsigned long long nv;
+        if (ep > P.gepoch) return false;
+        if (ep < P.gepoch) {
+            nv = (P.gepoch << GQ_SHIFT) | 1ull;
+            idx = 0;
+        } else {
+            if (cnt >= nstatic) return false;
+            nv = v + 1ull;
+            idx = cnt;
+        }
+        const unsigned long long old = atomicCAS_system(P.gqueue, v, nv);
+        if (old == v) return true;
+        v = old;
+    }
+}
 
 // ---------------------------------------------------------------- push filter
 // Push of u = stack[k] onto a stack of k members: filter level k (minus its
@@ -1561,16 +1606,16 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
         int kind = -1;  // -1 none, 0 static, 1 dynamic, 2 terminate
         unsigned long long idx = 0;
         if (lane == 0) {
-            const bool have_static = ld_volatile(&qs->static_next) < nstatic;
+            const bool have_static = statics_left(P, nstatic);
             const unsigned long long h0 = ld_volatile(&qs->head);
             const bool have_dyn = ld_volatile(&P.qstate[h0 % qcap]) == 2u * static_cast<unsigned int>(h0 / qcap) + 1u;
             if (have_static || have_dyn) {
                 // announce before claiming so that no waiter can observe
                 // busy == 0 while a claimed task is still unannounced
                 atomicAdd(&qs->busy, 1u);
-                if (have_static) {
-                    idx = atomicAdd(&qs->static_next, 1ull);
-                    if (idx < nstatic) kind = 0;
+                if (have_static && claim_static(P, nstatic, idx)) {
+                    kind = 0;
+                    atomicAdd(P.counters + C_STATIC, 1ull);
                 }
                 if (kind < 0) {
                     const unsigned long long h = ld_volatile(&qs->head);
@@ -1591,7 +1636,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                     backoff = 128;
                 }
                 if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
-                    ld_volatile(&qs->static_next) >= nstatic) {
+                    !statics_left(P, nstatic)) {
                     kind = 2;
                 } else if (clock64() - wait_t0 > (1ll << 35)) {
                     atomicOr(P.error_flag, 8);  // watchdog: ~17 s without work

@@ -3,12 +3,20 @@
 Replaces the reference's OpenMP pull queue (src/parallel.cpp:35-118) and the
 paper's MPI scheduler/worker split. The m-l+1 S1 l-mers are
 independent subproblems (split_subproblems, src/parallel.cpp:14-20) whose motif
-sets union to the answer; rank r searches offsets j with j % world == r on its
-own GPU (cost per S1 l-mer varies by ~±15%, so an interleaved
-split balances without a data-path collective). The one exchange step is the
-union of the per-rank motif sets: an allgather of counts, then an allgather of
-padded 128-bit key buffers (NCCL over NVLink on GPUs, gloo in the CPU tests),
-followed by the device sort+unique of pms8g_merge_keys.
+sets union to the answer. Two ways to split them over the ranks:
+
+* "queue" (default on GPUs): dynamic pull. Every rank builds the level-1 rows
+  of every S1 l-mer (microseconds) and claims (S1 l-mer, depth-1 branch) tasks,
+  heaviest first, from ONE epoch-tagged counter that lives in rank 0's HBM and
+  is mapped into every other rank's device over NVLink (pms8g_queue_*, CUDA
+  IPC) — the reference's shared next-job counter (src/parallel.cpp:54-60) at
+  node scale, with no data-path collective;
+* "static": rank r searches offsets j with j % world == r (pms8g_options.shard_*).
+
+The one exchange step is the union of the per-rank motif sets: an allgather of
+counts, then an allgather of padded 128-bit key buffers (NCCL over NVLink on
+GPUs, gloo in the CPU tests), followed by the device sort+unique of
+pms8g_merge_keys.
 """
 import ctypes
 from typing import Optional
@@ -31,6 +39,62 @@ def shard_offsets(num_offsets: int, rank: int, world: int):
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad shard {rank}/{world}")
     return [j for j in range(num_offsets) if j % world == rank]
+
+
+class SharedQueue:
+    """Host handle of a pms8g_queue: created on one rank, opened on the others
+    from its 64-byte IPC handle (the device memory stays on the creator)."""
+
+    def __init__(self, ptr, handle: bytes, owner: bool):
+        self.ptr, self.handle, self.owner = ptr, handle, owner
+
+    @staticmethod
+    def create(device: int = -1) -> "SharedQueue":
+        from . import _capi, _raise
+        q = ctypes.c_void_p()
+        h = (ctypes.c_uint8 * _capi.QUEUE_HANDLE_BYTES)()
+        err = ctypes.create_string_buffer(512)
+        rc = _capi.lib().pms8g_queue_create(device, ctypes.byref(q), h, err, len(err))
+        if rc != 0:
+            _raise(rc, err)
+        return SharedQueue(q.value, bytes(h), True)
+
+    @staticmethod
+    def open(handle: bytes, device: int = -1) -> "SharedQueue":
+        from . import _capi, _raise
+        if len(handle) != _capi.QUEUE_HANDLE_BYTES:
+            raise ValueError("bad queue handle")
+        q = ctypes.c_void_p()
+        h = (ctypes.c_uint8 * _capi.QUEUE_HANDLE_BYTES).from_buffer_copy(handle)
+        err = ctypes.create_string_buffer(512)
+        rc = _capi.lib().pms8g_queue_open(h, device, ctypes.byref(q), err, len(err))
+        if rc != 0:
+            _raise(rc, err)
+        return SharedQueue(q.value, handle, False)
+
+    def close(self):
+        from . import _capi
+        if self.ptr:
+            _capi.lib().pms8g_queue_destroy(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def shared_queue(device: int, group=None) -> SharedQueue:
+    """Collective: rank 0 of `group` creates the queue on its device and
+    broadcasts the IPC handle; every rank returns its own mapping."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    obj = [None]
+    q = None
+    if rank == 0:
+        q = SharedQueue.create(device)
+        obj[0] = q.handle
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    if rank != 0:
+        q = SharedQueue.open(obj[0], device)
+    dist.barrier(group)
+    return q
 
 
 def allgather_keys(local, group=None):
@@ -106,12 +170,14 @@ def device_keys_tensor(ptr: int, count: int):
 
 
 _CTX_CACHE = {}
+_QUEUES = {}
 
 
-def run_sharded(problem, config=None, options=None, report=None, group=None):
+def run_sharded(problem, config=None, options=None, report=None, group=None, split="queue"):
     """run_parallel across the ranks of torch.distributed: each rank searches
-    its shard on its GPU, then allgather + device merge; every rank returns
-    the full motif set."""
+    on its GPU — pulling tasks from the shared cross-GPU queue (split="queue")
+    or its interleaved shard (split="static") — then allgather + device merge;
+    every rank returns the full motif set."""
     import torch
     import torch.distributed as dist
     from . import Context, ParallelOptions, RunReport, _validated
@@ -120,8 +186,14 @@ def run_sharded(problem, config=None, options=None, report=None, group=None):
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     codes = _validated(problem)
     n, m = codes.shape
-    opts = dataclasses.replace(options, shard_rank=rank, shard_count=world,
-                               device=options.device if options.device >= 0 else torch.cuda.current_device())
+    device = options.device if options.device >= 0 else torch.cuda.current_device()
+    if split == "queue":
+        q = _QUEUES.get(group)
+        if q is None:
+            q = _QUEUES[group] = shared_queue(device, group)
+        opts = dataclasses.replace(options, shard_rank=0, shard_count=1, device=device, queue=q)
+    else:
+        opts = dataclasses.replace(options, shard_rank=rank, shard_count=world, device=device)
     # device contexts are cached per shape/options, like the library's own
     # handle cache for pms8g_solve
     key = (n, m, problem.motif_length, problem.max_mismatches, problem.alphabet.symbols, repr(config), repr(opts))

@@ -120,3 +120,17 @@ def test_no_cpu_fallback_without_gpu():
     inst = P.generate_planted_instance(P.PlantedInstanceSpec(l=13, d=4, seed=1, mutation=P.MutationMode.exactly_d))
     with pytest.raises(P.DeviceError, match="no CPU fallback"):
         P.solve(inst.problem)
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure mode")
+def test_scanner_has_no_cpu_fallback():
+    inst = P.generate_planted_instance(P.PlantedInstanceSpec(l=8, d=1, n=4, m=30, seed=1))
+    with pytest.raises(P.DeviceError, match="no CPU fallback"):
+        P.brute_force_solve(inst.problem)
+    with pytest.raises(P.DeviceError, match="no CPU fallback"):
+        P.verify_motifs(inst.problem, [inst.motif])
+    # argument errors are reported before any device work (Problem::validate, check_guard)
+    with pytest.raises(P.InvalidArgument, match="exceeds guard"):
+        P.brute_force_solve(inst.problem, enumeration_guard=1000)
+    with pytest.raises(P.InvalidArgument, match="expected l=8"):
+        P.verify_motifs(inst.problem, ["ACGT"])

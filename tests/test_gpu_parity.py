@@ -254,17 +254,42 @@ def test_gpu_threshold_rule():
         [2, 3, 3, 4, 5]
 
 
-def test_sharded_ranks_on_one_gpu_match_golden():
+@pytest.mark.parametrize("split", ["static", "queue"])
+def test_sharded_ranks_on_one_gpu_match_golden(split):
     # torchrun with 2 ranks sharing GPU 0 (keys exchanged with gloo): the
-    # per-rank shards, allgather and device merge give the full motif set
+    # per-rank shards (or the shared queue), allgather and device merge give
+    # the full motif set
     import sys
     env = dict(os.environ, PMS8G_SINGLE_GPU="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
-                        "--gpus", "2", "--config", "13_4", "--steps", "1", "--no-cpu-baseline"],
+                        "--gpus", "2", "--config", "13_4", "--steps", "1", "--no-cpu-baseline", "--split", split],
                        capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [x for x in r.stdout.splitlines() if x.startswith("{")][0]
     out = json.loads(line)
     assert out["n_gpus"] == 2
     assert out["motifs"] == golden("planted_13_4.json")[0]["motifs"]
+
+
+@pytest.mark.parametrize("world,l,d,seed", [(2, 13, 4, 2), (3, 17, 6, 1)])
+def test_shared_queue_ranks_claim_every_task_once(tmp_path, world, l, d, seed):
+    # ranks pull (S1 l-mer, branch) tasks from one epoch-tagged counter over
+    # several consecutive runs: each run's static claims sum to the task count
+    # of a single-device run (no task lost or repeated) and the merged motif
+    # set equals the reference's
+    import sys
+    out = tmp_path / "q.json"
+    env = dict(os.environ, PMS8G_SINGLE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+                        "--master-addr", "127.0.0.1", "--master-port", "29541",
+                        os.path.join(ROOT, "tests", "_queue_worker.py"), str(l), str(d), str(seed), "3", str(out)],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    want = [x for x in golden(f"planted_{l}_{d}.json") if x["seed"] == seed][0]["motifs"]
+    assert res["nstatic"] > 0
+    for run in res["runs"]:
+        assert run["motifs"] == want
+        assert run["statics"] == res["nstatic"]
+    assert res["api"] == want
