@@ -494,11 +494,12 @@ template <int W, int NCH>
 __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const uint32_t* entries, int st, int cnt,
                                          int n, int d, int lane, int& scanned) {
     Lmer<W> cd[NCH];
-    bool alive[NCH], hit[NCH];
+    bool alive[NCH];
+    int hm[NCH];  // smallest distance to the entries scanned so far (dead lanes: 0)
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         alive[ch] = ch * 32 + lane < n;
-        hit[ch] = false;
+        hm[ch] = alive[ch] ? 0x7fff : 0;
         if (alive[ch]) cd[ch] = cand[ch * 32 + lane];
     }
     constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
@@ -513,13 +514,14 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const Lmer<W> V = shfl_lmer<W>(mine, (x0 + u) & 31);
+                // XOR, XOR|OR, POPC, IMNMX per compare
 #pragma unroll
-                for (int ch = 0; ch < NCH; ++ch) hit[ch] |= dist<W>(cd[ch], V) <= d;
+                for (int ch = 0; ch < NCH; ++ch) hm[ch] = min(hm[ch], dist<W>(cd[ch], V));
             }
             scanned += U;
             bool all = true;
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) all &= hit[ch] || !alive[ch];
+            for (int ch = 0; ch < NCH; ++ch) all &= hm[ch] <= d;
             if (__all_sync(0xffffffffu, all)) {
                 done = true;
                 break;
@@ -530,7 +532,7 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
     int out = 0;
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
-        const bool keep = alive[ch] && hit[ch];
+        const bool keep = alive[ch] && hm[ch] <= d;
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (keep) cand[out + __popc(bal & lanemask_lt())] = cd[ch];
         out += __popc(bal);

@@ -16,7 +16,8 @@ anchors = list(range(0, 600 - l + 1, stride)) if stride > 1 else None
 shard = os.environ.get("SHARD")  # "r/N": interleaved shard r of N
 sr, sn = (int(x) for x in shard.split("/")) if shard else (0, 1)
 ctx = P.Context(20, 600, l, d, P.Alphabet.dna(), P.SolverConfig(threshold_override=t or None),
-                P.ParallelOptions(anchors=anchors, shard_rank=sr, shard_count=sn))
+                P.ParallelOptions(anchors=anchors, shard_rank=sr, shard_count=sn,
+                                  warps_per_block=int(os.environ.get("WARPS", "0"))))
 ctx.load_codes(inst.codes.ctypes.data, False)
 for r in range(reps):
     t0 = time.perf_counter()
