@@ -1113,9 +1113,10 @@ __device__ __noinline__ void prepare_tuple_fast(WarpCtx<1, MT>& C, int t, const 
 #pragma unroll
         for (int x = 0; x < 4; ++x) tr[x] = min(tr[x], 127u);
         uint4 w;
-        w.x = pr[0] | (pr[1] << 8) | (pr[2] << 16) | (pr[3] << 24);
-        w.y = pr[4] | (pr[5] << 8) | (cons << 16);
-        w.z = tr[0] | (tr[1] << 8) | (tr[2] << 16) | (tr[3] << 24);
+        // stored as 0x80 - threshold per byte (bytes <= 127: no borrows), see swar_feasible
+        w.x = 0x80808080u - (pr[0] | (pr[1] << 8) | (pr[2] << 16) | (pr[3] << 24));
+        w.y = 0x80808080u - (pr[4] | (pr[5] << 8) | (cons << 16));
+        w.z = 0x80808080u - (tr[0] | (tr[1] << 8) | (tr[2] << 16) | (tr[3] << 24));
         w.w = q == 0 ? 0u : static_cast<uint32_t>(q < 32 ? prevpos : lastpos);  // position of depth q - 1
         thr[q] = w;
     }
@@ -1168,32 +1169,34 @@ __device__ __forceinline__ bool expand_child_swar(const WarpCtx<W, MT>& C, const
 }
 
 
-// SWAR check of a child's budget bytes R against the suffix thresholds T of
-// its position (pairs, consensus, Theorem-1 triples), specialised on MT.
+// SWAR check of a child's budget bytes R against the suffix thresholds of
+// its position (pairs, consensus, Theorem-1 triples), specialised on MT. The
+// fast tables hold 0x80 - threshold per byte (prepare_tuple_fast), so
+// "sum >= threshold" is bit 7 of sum + (0x80 - threshold): every sum and
+// threshold is <= 127, so no byte carries into the next, and the three
+// words are checked with one AND. Sums are assembled with PRMT.
 template <int MT>
 __device__ __forceinline__ bool swar_feasible(uint32_t R, const uint4& T, int prune) {
-    if (MT == 2) {
-        const uint32_t s01 = (R + (R >> 8)) & 0xFFu;
-        return s01 >= (T.x & 0xFFu);
-    }
-    const uint32_t r3 = R >> 24;
-    const uint32_t A1 = R + (R >> 8);   // [01, 12, 23, 3]
-    const uint32_t A2 = R + (R >> 16);  // [02, 13, 2, 3]
-    const uint32_t P1 = (A1 & 0x00FFFFFFu) | (A2 << 24);
-    bool ok = bytes_ge(P1, T.x);
-    if (prune == 1) {
-        if (MT == 4) ok = ok && bytes_ge(((A2 >> 8) & 0xFFu) | (((R + r3) & 0xFFu) << 8), T.y & 0xFFFFu);
-        return ok;
-    }
-    const uint32_t S3 = A1 + (R >> 16);  // [012, 123, ...]
+    const uint32_t M = 0x80808080u;
+    const uint32_t A1 = R + (R >> 8);  // [01, 12, 23, 3]
+    if (MT == 2) return ((A1 + T.x) & 0x80u) != 0u;
+    const uint32_t R16 = R >> 16;
+    const uint32_t A2 = R + R16;                       // [02, 13, 2, 3]
+    const uint32_t P1 = __byte_perm(A1, A2, 0x4210);   // [01, 12, 23, 02]
+    const uint32_t S3 = A1 + R16;                      // [012, 123, ., .]
     if (MT == 3) {
         // pairs 01,12,02 + triple 012 (= the consensus bound for 3 members)
-        return ok && ((S3 & 0xFFu) >= (T.z & 0xFFu));
+        const uint32_t a = P1 + T.x;
+        return ((prune == 2 ? a & (S3 + T.z) : a) & M) == M;
     }
-    const uint32_t cons = (S3 + r3) & 0xFFu;
-    const uint32_t P2 = ((A2 >> 8) & 0xFFu) | (((R + r3) & 0xFFu) << 8) | (cons << 16);
-    const uint32_t T3 = (S3 & 0xFFFFu) | (((A1 + r3) & 0xFFu) << 16) | (((A2 + r3) & 0xFFu) << 24);
-    return ok && bytes_ge(P2, T.y) && bytes_ge(T3, T.z);
+    const uint32_t R24 = R >> 24;
+    const uint32_t B = R + R24;                              // [03, ...]
+    const uint32_t X = __byte_perm(A2, B, 0x0041);           // [13, 03, ., .]
+    const uint32_t P2 = __byte_perm(X, S3 + R24, 0x0410);    // [13, 03, 0123, 13]
+    if (prune == 1) return ((P1 + T.x) & (P2 + ((T.y & 0xFFFFu) | 0x80800000u)) & M) == M;
+    const uint32_t Y = __byte_perm(A1 + R24, A2 + R24, 0x0040);  // [013, 023, ., .]
+    const uint32_t T3 = __byte_perm(S3, Y, 0x5410);              // [012, 123, 013, 023]
+    return ((P1 + T.x) & (P2 + T.y) & (T3 + T.z) & M) == M;
 }
 
 // Enumeration loop for l <= 32 and t <= 4: nodes are uint4 {h, o, budgets,
