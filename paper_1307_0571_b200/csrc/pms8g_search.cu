@@ -519,10 +519,10 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
                 for (int ch = 0; ch < NCH; ++ch) hm[ch] = min(hm[ch], dist<W>(cd[ch], V));
             }
             scanned += U;
-            bool all = true;
+            int mx = hm[0];
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) all &= hm[ch] <= d;
-            if (__all_sync(0xffffffffu, all)) {
+            for (int ch = 1; ch < NCH; ++ch) mx = max(mx, hm[ch]);
+            if (__all_sync(0xffffffffu, mx <= d)) {
                 done = true;
                 break;
             }
