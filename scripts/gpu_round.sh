@@ -1,8 +1,13 @@
+# Round measurement pass: GPU tests, bench lines for every config, the
+# reference arm, the ncu launch list and one ncu --set full capture of the
+# (17,6) search kernel.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-timeout 900 bash scripts/bench_all.sh r01b > gpurun_out/bench_all.log 2>&1
+timeout 900 bash scripts/bench_all.sh ${TAG:-r01c} > gpurun_out/bench_all.log 2>&1
 timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_17_6.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:search_kernel -c 1 \
+  -o gpurun_out/search_17_6_full -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo done
