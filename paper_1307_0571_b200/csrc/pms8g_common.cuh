@@ -54,9 +54,11 @@ __device__ __forceinline__ int suffix_popc(const Mask<W>& m, int p) {
     int s = 0;
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-        const int lo = p - 32 * i;  // bits of word i at index >= lo
-        if (lo <= 0) s += __popc(m.w[i]);
-        else if (lo < 32) s += __popc(m.w[i] >> lo);
+        // bits of word i at index >= p - 32i; branch-free (lanes hold
+        // different p): the clamped funnel shift gives 0 once the shift
+        // reaches 32
+        const int lo = max(p - 32 * i, 0);
+        s += __popc(__funnelshift_rc(m.w[i], 0u, static_cast<unsigned>(lo)));
     }
     return s;
 }

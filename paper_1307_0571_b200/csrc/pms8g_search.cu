@@ -659,6 +659,11 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
         __syncwarp();
         return;
     }
+    // members in registers (Tm lives on the stack: its address crosses calls)
+    Lmer<W> tm[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+        if (i < t) tm[i] = Tm[i];
     int key[NC];
     unsigned present = 0u;
 #pragma unroll
@@ -670,7 +675,7 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
 #pragma unroll
             for (int i = 0; i < MT; ++i)
                 if (i < t) {
-                    const int ci = code_at<W>(Tm[i], p);
+                    const int ci = code_at<W>(tm[i], p);
 #pragma unroll
                     for (int x = 0; x < 4; ++x) f[x] += ci == x;
                 }
@@ -718,7 +723,7 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
         const int pos = q < l ? S.perm[q] : 0;
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-            const int code = (i < t && q < l) ? code_at<W>(Tm[i], pos) : 0;
+            const int code = (i < t && q < l) ? code_at<W>(tm[i], pos) : 0;
             nh[i][c] = __ballot_sync(0xffffffffu, (code >> 1) & 1);
             no[i][c] = __ballot_sync(0xffffffffu, code & 1);
         }
@@ -742,12 +747,18 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
     const int lane = C.lane, l = P.l;
     WarpFixed& S = *C.S();
     const int np = P.plan.npair, ntot = P.plan.npair + P.plan.ntri;
+    // members and their pairwise mismatch masks in registers (Tm lives on
+    // the stack: its address crosses calls)
+    Lmer<W> tm[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+        if (i < t) tm[i] = Tm[i];
     for (int p = lane; p <= l; p += 32) {
         uint32_t e = 0;
         if (p < l) {
 #pragma unroll
             for (int i = 0; i < MT; ++i)
-                if (i < t) e |= 1u << (8 * code_at<W>(Tm[i], p) + i);
+                if (i < t) e |= 1u << (8 * code_at<W>(tm[i], p) + i);
             gen_eq(C)[p] = e;
         }
         uint8_t* row = C.thr() + GEN_TBL_BYTES + p * ntot;
@@ -755,7 +766,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
         for (int j = 1; j < MT; ++j)
 #pragma unroll
             for (int i = 0; i < j; ++i)
-                if (j < t) row[j * (j - 1) / 2 + i] = static_cast<uint8_t>(suffix_popc<W>(mism<W>(Tm[i], Tm[j]), p));
+                if (j < t) row[j * (j - 1) / 2 + i] = static_cast<uint8_t>(suffix_popc<W>(mism<W>(tm[i], tm[j]), p));
 #pragma unroll
         for (int h = 2; h < MT; ++h)
 #pragma unroll
@@ -763,9 +774,9 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
 #pragma unroll
                 for (int i = 0; i < j; ++i)
                     if (h < t) {
-                        const Mask<W> mij = mism<W>(Tm[i], Tm[j]);
-                        const Mask<W> mih = mism<W>(Tm[i], Tm[h]);
-                        const Mask<W> mjh = mism<W>(Tm[j], Tm[h]);
+                        const Mask<W> mij = mism<W>(tm[i], tm[j]);
+                        const Mask<W> mih = mism<W>(tm[i], tm[h]);
+                        const Mask<W> mjh = mism<W>(tm[j], tm[h]);
                         Mask<W> n4;
 #pragma unroll
                         for (int x = 0; x < W; ++x) n4.w[x] = mij.w[x] & mih.w[x] & mjh.w[x];
