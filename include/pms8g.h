@@ -65,6 +65,7 @@ typedef struct pms8g_options {
                                 id seq*(m-l+1)+offset of an l-mer in that S1 l-mer's branching row);
                                 the result is the motif set under those branches only */
     int nbranches;
+    int grid_blocks;       /* persistent grid of the search kernel; 0: one block per SM x blocks_per_sm */
     pms8g_queue* queue;    /* optional shared queue (multi-GPU dynamic pull over S1 l-mers, replacing the
                               reference's shared atomic job counter src/parallel.cpp:54-60 across GPUs):
                               every rank searches all S1 l-mers, claiming (S1 l-mer, depth-1 branch) tasks
@@ -109,6 +110,14 @@ void pms8g_default_options(pms8g_options* opt);
 int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt,
                 pms8g_result* out, char* err, size_t errlen);
 void pms8g_result_free(pms8g_result* r);
+
+/* Several instances of one shape (the paper averages 5 seeds per (l,d)),
+ * searched concurrently on one device: each in-flight instance gets an equal share of the
+ * SMs (its own persistent grid) and stream; results are per instance, like pms8g_solve
+ * (no reference counterpart: the reference solves one Problem per run_parallel call).
+ * report.wall_seconds is the batch wall time. */
+int pms8g_solve_batch(const uint8_t* const* codes, int count, int n, int m, int l, int d, const char* alphabet,
+                      const pms8g_options* opt, pms8g_result* outs, char* err, size_t errlen);
 
 /* Device-resident context: allocate once, load codes (host or device pointer),
  * run many times. Keys: 128-bit MSB-first 2-bit packing of each motif (symbol

@@ -35,7 +35,7 @@ __all__ = [
     "MotifSet", "solve", "run_parallel", "split_subproblems", "resolve_worker_count", "generate_planted_instance",
     "PlantedInstanceSpec", "PlantedInstance", "MutationMode", "estimate_threshold", "gpu_threshold",
     "InvalidArgument", "SolverRuntimeError", "SolverLogicError", "DeviceError", "ExtensionMissing", "Context",
-    "canonical_motif_set", "naive_is_motif", "verify_motifs", "brute_force_solve",
+    "canonical_motif_set", "naive_is_motif", "verify_motifs", "brute_force_solve", "solve_batch",
 ]
 
 MotifSet = List[str]
@@ -191,6 +191,7 @@ class ParallelOptions:
     warps_per_block: int = 0
     blocks_per_sm: int = 0
     exact_tree: bool = False  # True: same search tree as the reference (every row filtered at every push)
+    grid_blocks: int = 0  # persistent grid of the search kernel (0: one block per SM)
     branches: Optional[Sequence] = None  # explicit depth-1 branches [(s1_offset, seq, offset), ...]
     queue: Optional[object] = None  # parallel.SharedQueue: cross-GPU dynamic pull (exclusive with shard_count > 1)
     split: str = "queue"  # run_parallel under torch.distributed: "queue" (shared cross-GPU queue) or "static"
@@ -273,6 +274,7 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions], win
     o.warps_per_block = int(par.warps_per_block)
     o.blocks_per_sm = int(par.blocks_per_sm)
     o.exact_tree = 1 if par.exact_tree else 0
+    o.grid_blocks = int(par.grid_blocks)
     if par.queue is not None:
         o.queue = par.queue.ptr
     keep = None
@@ -410,6 +412,49 @@ def brute_force_solve(problem: Problem, enumeration_guard: int = 1000000, report
     finally:
         L.pms8g_result_free(ctypes.byref(res))
     return motifs
+
+
+def solve_batch(problems: Sequence[Problem], config: Optional[SolverConfig] = None,
+                options: Optional[ParallelOptions] = None,
+                reports: Optional[List[RunReport]] = None) -> List[MotifSet]:
+    """Several instances of one shape searched concurrently on one GPU
+    (pms8g_solve_batch): each in-flight instance gets an equal share of the
+    SMs. Returns one sorted motif set per problem, as solve() would."""
+    if not problems:
+        return []
+    p0 = problems[0]
+    codes = []
+    for pr in problems:
+        c = _validated(pr)
+        if (pr.n(), pr.m(), pr.motif_length, pr.max_mismatches, pr.alphabet.symbols) != \
+                (p0.n(), p0.m(), p0.motif_length, p0.max_mismatches, p0.alphabet.symbols):
+            raise InvalidArgument("solve_batch: every problem must have the same n, m, l, d and alphabet")
+        codes.append(c)
+    n, m = codes[0].shape
+    l = p0.motif_length
+    o, keep = _options(config, options, m - l + 1)
+    ptrs = (ctypes.c_void_p * len(codes))(*[c.ctypes.data for c in codes])
+    res = (_capi.Result * len(codes))()
+    err = ctypes.create_string_buffer(512)
+    L = _capi.lib()
+    rc = L.pms8g_solve_batch(ptrs, len(codes), n, m, l, p0.max_mismatches, p0.alphabet.symbols.encode(),
+                             ctypes.byref(o), res, err, len(err))
+    del keep
+    if rc != 0:
+        _raise(rc, err)
+    out = []
+    try:
+        for i, r in enumerate(res):
+            raw = ctypes.string_at(r.motifs, r.count * r.l).decode() if r.count else ""
+            out.append([raw[k * l:(k + 1) * l] for k in range(r.count)])
+            if reports is not None:
+                rep = RunReport()
+                rep.fill(r.report, p0.alphabet.name())
+                reports.append(rep)
+    finally:
+        for r in res:
+            L.pms8g_result_free(ctypes.byref(r))
+    return out
 
 
 def split_subproblems(problem: Problem):

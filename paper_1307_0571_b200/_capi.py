@@ -34,6 +34,7 @@ class Options(ctypes.Structure):
         ("exact_tree", ctypes.c_int),
         ("branches", ctypes.POINTER(ctypes.c_int32)),
         ("nbranches", ctypes.c_int),
+        ("grid_blocks", ctypes.c_int),
         ("queue", ctypes.c_void_p),
     ]
 
@@ -71,7 +72,7 @@ EXPORTS = [
     "pms8g_ctx_counters",
     "pms8g_ctx_destroy", "pms8g_merge_keys", "pms8g_decode_keys", "pms8g_generate", "pms8g_estimate_threshold",
     "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version", "pms8g_verify_motifs", "pms8g_brute_force",
-    "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy",
+    "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy", "pms8g_solve_batch",
 ]
 QUEUE_HANDLE_BYTES = 64
 
@@ -140,6 +141,9 @@ def lib():
     L.pms8g_queue_open.restype = c_int
     L.pms8g_queue_destroy.argtypes = [c_vp]
     L.pms8g_queue_destroy.restype = None
+    L.pms8g_solve_batch.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options),
+                                    ctypes.POINTER(Result), c_char_p, c_sz]
+    L.pms8g_solve_batch.restype = c_int
     L.pms8g_version.argtypes = []
     L.pms8g_version.restype = c_char_p
     _lib = L

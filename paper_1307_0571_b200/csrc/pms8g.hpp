@@ -75,6 +75,9 @@ struct RunReport {
 MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const GpuOptions& options,
                       RunReport* report = nullptr);
 MotifSet solve(const Problem& problem, const SolverConfig& config = {}, RunReport* report = nullptr);
+// Instances of one shape searched concurrently on one device (pms8g_solve_batch).
+std::vector<MotifSet> solve_batch(const std::vector<Problem>& problems, const SolverConfig& config = {},
+                                  int device = -1);
 
 struct SequenceFile {
     std::vector<std::string> names;

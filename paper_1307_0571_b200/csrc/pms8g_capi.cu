@@ -20,6 +20,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pms8g.h"
@@ -482,7 +483,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
                                  "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K, smem_cap));
     c->warps = warps;
     c->smem = search_smem(c->W, c->K, warps, c->plan);
-    c->blocks = c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
+    c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
     if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
 
@@ -677,6 +678,8 @@ int pms8g_merge_keys(const uint64_t* dev_in, int64_t count, uint64_t* dev_out, i
 namespace {
 std::mutex g_cache_mu;
 pms8g_ctx* g_cache = nullptr;
+std::mutex g_batch_mu;
+std::vector<pms8g_ctx*> g_batch;  // pms8g_solve_batch's lane contexts
 
 bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alphabet, const pms8g_options& o) {
     if (!c) return false;
@@ -689,7 +692,8 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
            c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
            (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && o.branches == nullptr &&
            c->opt.warps_per_block == o.warps_per_block &&
-           c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree && c->opt.queue == o.queue;
+           c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree && c->opt.queue == o.queue &&
+           c->opt.grid_blocks == o.grid_blocks;
 }
 }  // namespace
 
@@ -725,6 +729,85 @@ int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* al
     if (!cached) pms8g_ctx_destroy(c);
     if (!rc) out->report.wall_seconds = now_s() - t0;
     return rc;
+}
+
+int pms8g_solve_batch(const uint8_t* const* codes, int count, int n, int m, int l, int d, const char* alphabet,
+                      const pms8g_options* opt_in, pms8g_result* outs, char* err, size_t errlen) {
+    const double t0 = now_s();
+    if (count < 0) return fail(err, errlen, PMS8G_ERR_INVALID, "negative instance count");
+    for (int i = 0; i < count; ++i) std::memset(&outs[i], 0, sizeof outs[i]);
+    if (count == 0) return PMS8G_OK;
+    pms8g_options opt;
+    if (opt_in) opt = *opt_in;
+    else pms8g_default_options(&opt);
+    if (opt.queue) return fail(err, errlen, PMS8G_ERR_INVALID, "a batch runs on one device: no shared queue");
+    int sigma = 0;
+    int rc = validate_problem(n, m, l, d, alphabet, err, errlen, &sigma);
+    if (rc) return rc;
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(err, errlen, PMS8G_ERR_CUDA, "no CUDA device available (%s); the GPU path has no CPU fallback",
+                    cudaGetErrorString(ce));
+    int dev = opt.device;
+    if (dev < 0) CU(cudaGetDevice(&dev));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // up to `lanes` instances in flight, each on its own stream with an equal
+    // share of the SMs (its persistent grid), one host thread each; waves of
+    // `lanes` when there are more instances than that
+    const int lanes = std::max(1, std::min({count, sms, opt.grid_blocks > 0 ? sms / opt.grid_blocks : 8}));
+    opt.device = dev;
+    opt.grid_blocks = std::max(1, sms / lanes);
+    // the lanes' contexts are cached across calls of the same shape (like
+    // pms8g_solve's handle cache); subset runs are never cached
+    std::lock_guard<std::mutex> lock(g_batch_mu);
+    const bool cacheable = !opt.anchors && !opt.branches;
+    bool reuse = cacheable && static_cast<int>(g_batch.size()) == lanes;
+    for (int k = 0; reuse && k < lanes; ++k) reuse = same_shape(g_batch[k], n, m, l, d, alphabet, opt);
+    if (!reuse) {
+        for (auto* c : g_batch) pms8g_ctx_destroy(c);
+        g_batch.clear();
+    }
+    std::vector<pms8g_ctx*> ctx = reuse ? g_batch : std::vector<pms8g_ctx*>(lanes, nullptr);
+    for (int k = 0; !reuse && k < lanes; ++k)
+        if ((rc = pms8g_ctx_create(n, m, l, d, alphabet, &opt, &ctx[k], err, errlen))) {
+            for (auto* c : ctx) pms8g_ctx_destroy(c);
+            return rc;
+        }
+    if (cacheable) g_batch = ctx;
+    std::vector<int> rcs(count, PMS8G_OK);
+    std::vector<std::string> msgs(count);
+    for (int base = 0; base < count && rc == PMS8G_OK; base += lanes) {
+        const int nw = std::min(lanes, count - base);
+        std::vector<std::thread> th;
+        for (int k = 0; k < nw; ++k)
+            th.emplace_back([&, k] {
+                const int i = base + k;
+                char e[512] = {0};
+                int r = cudaSetDevice(dev) == cudaSuccess ? PMS8G_OK : PMS8G_ERR_CUDA;
+                if (!r) r = pms8g_ctx_load_codes(ctx[k], codes[i], 0, e, sizeof e);
+                if (!r) r = pms8g_ctx_run(ctx[k], e, sizeof e);
+                if (!r) r = pms8g_ctx_result(ctx[k], &outs[i], e, sizeof e);
+                rcs[i] = r;
+                msgs[i] = e;
+            });
+        for (auto& x : th) x.join();
+        for (int k = 0; k < nw; ++k)
+            if (rcs[base + k] != PMS8G_OK && rc == PMS8G_OK) {
+                rc = fail(err, errlen, rcs[base + k], "instance %d: %s", base + k, msgs[base + k].c_str());
+            }
+    }
+    if (!cacheable) {
+        for (auto* c : ctx) pms8g_ctx_destroy(c);
+    }
+    if (rc != PMS8G_OK) {
+        for (int i = 0; i < count; ++i) pms8g_result_free(&outs[i]);
+        return rc;
+    }
+    const double wall = now_s() - t0;
+    for (int i = 0; i < count; ++i) outs[i].report.wall_seconds = wall;
+    return PMS8G_OK;
 }
 
 int pms8g_int_peak(int device, double* ops_per_second, double* popc_per_second, char* err, size_t errlen) {

@@ -198,6 +198,42 @@ MotifSet solve(const Problem& problem, const SolverConfig& config, RunReport* re
 
 SequenceFile read_plain(const std::string& path) { return parse_plain(slurp(path)); }
 
+std::vector<MotifSet> solve_batch(const std::vector<Problem>& problems, const SolverConfig& config, int device) {
+    std::vector<MotifSet> out(problems.size());
+    if (problems.empty()) return out;
+    const Problem& p0 = problems[0];
+    std::vector<std::vector<uint8_t>> codes;
+    std::vector<const uint8_t*> ptrs;
+    for (const auto& p : problems) {
+        p.validate();
+        if (p.n() != p0.n() || p.m() != p0.m() || p.motif_length != p0.motif_length ||
+            p.max_mismatches != p0.max_mismatches || p.alphabet != p0.alphabet)
+            throw std::invalid_argument("solve_batch: every problem must have the same n, m, l, d and alphabet");
+        codes.emplace_back();
+        for (const auto& s : p.sequences)
+            for (char ch : s) codes.back().push_back(static_cast<uint8_t>(p.alphabet.find(ch)));
+    }
+    for (const auto& c : codes) ptrs.push_back(c.data());
+    pms8g_options o;
+    pms8g_default_options(&o);
+    if (config.threshold_override) o.threshold = *config.threshold_override;
+    o.sort_rows = config.sort_rows ? 1 : 0;
+    o.prune_level = static_cast<int>(config.prune_level);
+    o.reverify = config.reverify_against_originals ? 1 : 0;
+    if (config.max_motifs) o.max_motifs = *config.max_motifs;
+    o.device = device;
+    std::vector<pms8g_result> res(problems.size());
+    char err[512] = {0};
+    const int rc = pms8g_solve_batch(ptrs.data(), static_cast<int>(ptrs.size()), p0.n(), p0.m(), p0.motif_length,
+                                     p0.max_mismatches, p0.alphabet.c_str(), &o, res.data(), err, sizeof err);
+    if (rc != PMS8G_OK) rethrow(rc, err);
+    for (size_t i = 0; i < res.size(); ++i) {
+        for (int64_t k = 0; k < res[i].count; ++k) out[i].emplace_back(res[i].motifs + k * res[i].l, res[i].l);
+        pms8g_result_free(&res[i]);
+    }
+    return out;
+}
+
 namespace {
 std::vector<uint8_t> encode_codes(const std::vector<std::string>& seqs, const std::string& alphabet) {
     std::vector<uint8_t> codes;

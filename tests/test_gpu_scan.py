@@ -138,3 +138,21 @@ def _codes_from_fasta(path):
     if cur:
         seqs.append("".join(cur))
     return O.codes_of(seqs)
+
+
+# ---------------------------------------------------------------- batching
+def test_solve_batch_matches_reference_per_instance():
+    # the paper's protocol: several instances per (l,d), here
+    # searched concurrently on one GPU, each with its share of the SMs
+    for l, d, seeds in ((13, 4, [1, 2, 3, 4, 5]), (17, 6, [1, 2, 3])):
+        gold = {g["seed"]: g["motifs"] for g in golden(f"planted_{l}_{d}.json")}
+        probs = [planted(l, d, s).problem for s in seeds]
+        reps = []
+        got = P.solve_batch(probs, reports=reps)
+        assert got == [gold[s] for s in seeds]
+        assert len(reps) == len(seeds) and all(r.subproblems == 600 - l + 1 for r in reps)
+    # more instances than concurrent lanes (waves) and a subset option
+    probs = [planted(13, 4, s).problem for s in [1, 2, 3, 4, 5] * 2]
+    got = P.solve_batch(probs, options=P.ParallelOptions(grid_blocks=37))
+    gold = {g["seed"]: g["motifs"] for g in golden("planted_13_4.json")}
+    assert got == [gold[s] for s in [1, 2, 3, 4, 5] * 2]

@@ -60,3 +60,13 @@ def test_shard_offsets_partition():
 
 def test_canonical_motif_set():
     assert P.canonical_motif_set(["CA", "AC", "CA", "AA"]) == ["AA", "AC", "CA"]
+
+
+def test_solve_batch_rejects_mixed_shapes():
+    import paper_1307_0571_b200 as P
+    a = P.Problem(["ACGTACGTAC", "ACGTACGTAA"], 5, 1)
+    b = P.Problem(["ACGTACGTAC", "ACGTACGTAA"], 6, 1)
+    import pytest
+    with pytest.raises(P.InvalidArgument, match="same n, m, l, d"):
+        P.solve_batch([a, b])
+    assert P.solve_batch([]) == []
