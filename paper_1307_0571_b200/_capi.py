@@ -141,9 +141,10 @@ def lib():
     L.pms8g_queue_open.restype = c_int
     L.pms8g_queue_destroy.argtypes = [c_vp]
     L.pms8g_queue_destroy.restype = None
-    L.pms8g_solve_batch.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options),
-                                    ctypes.POINTER(Result), c_char_p, c_sz]
-    L.pms8g_solve_batch.restype = c_int
+    if hasattr(L, "pms8g_solve_batch"):  # (older builds are loadable for A/B timing)
+        L.pms8g_solve_batch.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options),
+                                        ctypes.POINTER(Result), c_char_p, c_sz]
+        L.pms8g_solve_batch.restype = c_int
     L.pms8g_version.argtypes = []
     L.pms8g_version.restype = c_char_p
     _lib = L

@@ -54,11 +54,16 @@ __device__ __forceinline__ int suffix_popc(const Mask<W>& m, int p) {
     int s = 0;
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-        // bits of word i at index >= p - 32i; branch-free (lanes hold
-        // different p): the clamped funnel shift gives 0 once the shift
-        // reaches 32
-        const int lo = max(p - 32 * i, 0);
-        s += __popc(__funnelshift_rc(m.w[i], 0u, static_cast<unsigned>(lo)));
+        const int lo = p - 32 * i;  // bits of word i at index >= lo
+        if (W == 1) {
+            if (lo <= 0) s += __popc(m.w[i]);
+            else if (lo < 32) s += __popc(m.w[i] >> lo);
+        } else {
+            // branch-free for two-word l-mers (lanes hold different p and
+            // straddle the word boundary): the clamped funnel shift gives 0
+            // once the shift reaches 32
+            s += __popc(__funnelshift_rc(m.w[i], 0u, static_cast<unsigned>(max(lo, 0))));
+        }
     }
     return s;
 }

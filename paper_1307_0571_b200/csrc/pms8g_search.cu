@@ -659,11 +659,16 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
         __syncwarp();
         return;
     }
-    // members in registers (Tm lives on the stack: its address crosses calls)
-    Lmer<W> tm[MT];
+    // two-word members in registers (Tm lives on the stack: its address
+    // crosses calls); one-word builds read it in place (their register
+    // budget is shared with the fast loop)
+    Lmer<W> tm_r[MT];
+    if constexpr (W == 2) {
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
-        if (i < t) tm[i] = Tm[i];
+        for (int i = 0; i < MT; ++i)
+            if (i < t) tm_r[i] = Tm[i];
+    }
+    const Lmer<W>* tm = W == 2 ? tm_r : Tm;
     int key[NC];
     unsigned present = 0u;
 #pragma unroll
@@ -747,12 +752,14 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
     const int lane = C.lane, l = P.l;
     WarpFixed& S = *C.S();
     const int np = P.plan.npair, ntot = P.plan.npair + P.plan.ntri;
-    // members and their pairwise mismatch masks in registers (Tm lives on
-    // the stack: its address crosses calls)
-    Lmer<W> tm[MT];
+    // two-word members in registers (see order_positions)
+    Lmer<W> tm_r[MT];
+    if constexpr (W == 2) {
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
-        if (i < t) tm[i] = Tm[i];
+        for (int i = 0; i < MT; ++i)
+            if (i < t) tm_r[i] = Tm[i];
+    }
+    const Lmer<W>* tm = W == 2 ? tm_r : Tm;
     for (int p = lane; p <= l; p += 32) {
         uint32_t e = 0;
         if (p < l) {
