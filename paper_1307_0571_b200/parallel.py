@@ -79,20 +79,48 @@ class SharedQueue:
             self.ptr = None
 
 
-def shared_queue(device: int, group=None) -> SharedQueue:
+def shared_queue(device: int, group=None) -> Optional[SharedQueue]:
     """Collective: rank 0 of `group` creates the queue on its device and
-    broadcasts the IPC handle; every rank returns its own mapping."""
+    broadcasts the IPC handle; every rank returns its own mapping. Returns
+    None on every rank when some rank cannot map it with peer access (then
+    the caller falls back to the static split)."""
+    import torch
     import torch.distributed as dist
     rank = dist.get_rank(group)
     obj = [None]
-    q = None
+    q, ok = None, 1
     if rank == 0:
-        q = SharedQueue.create(device)
-        obj[0] = q.handle
+        try:
+            q = SharedQueue.create(device)
+            obj[0] = (q.handle, device)
+        except Exception:
+            ok = 0
     src = dist.get_global_rank(group, 0) if group is not None else 0
     dist.broadcast_object_list(obj, src=src, group=group)
     if rank != 0:
-        q = SharedQueue.open(obj[0], device)
+        if obj[0] is None:
+            ok = 0
+        else:
+            handle, dev0 = obj[0]
+            try:
+                # claims are system-scope atomics on rank 0's HBM: they need
+                # peer access (NVLink); several ranks on one device map it too
+                if dev0 != device and not torch.cuda.can_device_access_peer(device, dev0):
+                    raise RuntimeError("no peer access")
+                q = SharedQueue.open(handle, device)
+            except Exception:
+                ok = 0
+    dev = "cpu" if dist.get_backend(group) == "gloo" else torch.device("cuda", device)
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:
+        dist.barrier(group)
+        if q is not None and not q.owner:
+            q.close()
+        dist.barrier(group)
+        if q is not None and q.owner:
+            q.close()
+        return None
     dist.barrier(group)
     return q
 
@@ -187,12 +215,14 @@ def run_sharded(problem, config=None, options=None, report=None, group=None, spl
     codes = _validated(problem)
     n, m = codes.shape
     device = options.device if options.device >= 0 else torch.cuda.current_device()
+    q = None
     if split == "queue":
-        q = _QUEUES.get(group)
-        if q is None:
-            q = _QUEUES[group] = shared_queue(device, group)
+        if group not in _QUEUES:
+            _QUEUES[group] = shared_queue(device, group)
+        q = _QUEUES[group]
+    if q is not None:
         opts = dataclasses.replace(options, shard_rank=0, shard_count=1, device=device, queue=q)
-    else:
+    else:  # static split (requested, or no peer-mapped queue on this node)
         opts = dataclasses.replace(options, shard_rank=rank, shard_count=world, device=device)
     # device contexts are cached per shape/options, like the library's own
     # handle cache for pms8g_solve

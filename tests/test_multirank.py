@@ -85,3 +85,24 @@ def test_allgather_keys_variable_lengths(tmp_path):
     got = np.load(out)
     assert got.shape == (2, 2)
     assert (got == np.arange(4).reshape(2, 2)).all()
+
+
+def _queue_fallback_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1307_0571_b200.parallel import shared_queue
+        q = shared_queue(0)  # no device here: every rank must agree on None (static split)
+        with open(f"{out_path}.{rank}", "w") as f:
+            f.write("none" if q is None else "queue")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_queue_falls_back_together(tmp_path):
+    # the collective that maps rank 0's claim counter into every GPU: when a
+    # rank cannot map it, all ranks get None and use the static split
+    out = str(tmp_path / "q")
+    mp.spawn(_queue_fallback_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert [open(f"{out}.{r}").read() for r in range(2)] == ["none", "none"]
