@@ -668,7 +668,9 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
         for (int i = 0; i < MT; ++i)
             if (i < t) tm_r[i] = Tm[i];
     }
-    const Lmer<W>* tm = W == 2 ? tm_r : Tm;
+    // (indexed with unrolled constants, so tm_r stays in registers; a pointer
+    // to it would put it back on the stack)
+#define PMS8G_TM(i) (W == 2 ? tm_r[i] : Tm[i])
     int key[NC];
     unsigned present = 0u;
 #pragma unroll
@@ -680,7 +682,7 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
 #pragma unroll
             for (int i = 0; i < MT; ++i)
                 if (i < t) {
-                    const int ci = code_at<W>(tm[i], p);
+                    const int ci = code_at<W>(PMS8G_TM(i), p);
 #pragma unroll
                     for (int x = 0; x < 4; ++x) f[x] += ci == x;
                 }
@@ -728,7 +730,7 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
         const int pos = q < l ? S.perm[q] : 0;
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-            const int code = (i < t && q < l) ? code_at<W>(tm[i], pos) : 0;
+            const int code = (i < t && q < l) ? code_at<W>(PMS8G_TM(i), pos) : 0;
             nh[i][c] = __ballot_sync(0xffffffffu, (code >> 1) & 1);
             no[i][c] = __ballot_sync(0xffffffffu, code & 1);
         }
@@ -741,6 +743,8 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
             Tm[i].o[c] = no[i][c];
         }
 }
+
+#undef PMS8G_TM
 
 // Per-tuple suffix tables (NeighborhoodEnumerator::prepare, :164-226):
 // eq[p] (members holding each symbol), pair suffix distances, Theorem-1
@@ -759,13 +763,15 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
         for (int i = 0; i < MT; ++i)
             if (i < t) tm_r[i] = Tm[i];
     }
-    const Lmer<W>* tm = W == 2 ? tm_r : Tm;
+    // (indexed with unrolled constants, so tm_r stays in registers; a pointer
+    // to it would put it back on the stack)
+#define PMS8G_TM(i) (W == 2 ? tm_r[i] : Tm[i])
     for (int p = lane; p <= l; p += 32) {
         uint32_t e = 0;
         if (p < l) {
 #pragma unroll
             for (int i = 0; i < MT; ++i)
-                if (i < t) e |= 1u << (8 * code_at<W>(tm[i], p) + i);
+                if (i < t) e |= 1u << (8 * code_at<W>(PMS8G_TM(i), p) + i);
             gen_eq(C)[p] = e;
         }
         uint8_t* row = C.thr() + GEN_TBL_BYTES + p * ntot;
@@ -773,7 +779,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
         for (int j = 1; j < MT; ++j)
 #pragma unroll
             for (int i = 0; i < j; ++i)
-                if (j < t) row[j * (j - 1) / 2 + i] = static_cast<uint8_t>(suffix_popc<W>(mism<W>(tm[i], tm[j]), p));
+                if (j < t) row[j * (j - 1) / 2 + i] = static_cast<uint8_t>(suffix_popc<W>(mism<W>(PMS8G_TM(i), PMS8G_TM(j)), p));
 #pragma unroll
         for (int h = 2; h < MT; ++h)
 #pragma unroll
@@ -781,9 +787,9 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
 #pragma unroll
                 for (int i = 0; i < j; ++i)
                     if (h < t) {
-                        const Mask<W> mij = mism<W>(tm[i], tm[j]);
-                        const Mask<W> mih = mism<W>(tm[i], tm[h]);
-                        const Mask<W> mjh = mism<W>(tm[j], tm[h]);
+                        const Mask<W> mij = mism<W>(PMS8G_TM(i), PMS8G_TM(j));
+                        const Mask<W> mih = mism<W>(PMS8G_TM(i), PMS8G_TM(h));
+                        const Mask<W> mjh = mism<W>(PMS8G_TM(j), PMS8G_TM(h));
                         Mask<W> n4;
 #pragma unroll
                         for (int x = 0; x < W; ++x) n4.w[x] = mij.w[x] & mih.w[x] & mjh.w[x];
@@ -793,6 +799,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
                     }
     }
     __syncwarp();
+#undef PMS8G_TM
     int carry = 0;
     const int nchunk = (l + 32) / 32;
     for (int ch = nchunk - 1; ch >= 0; --ch) {
