@@ -477,8 +477,8 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
     c->plan = make_plan(c->W, l, t);
     int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
-    while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) > smem_cap) --warps;
-    if (search_smem(c->W, c->K, warps, c->plan) > smem_cap)
+    while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap) --warps;  // + static smem (TMA barrier)
+    if (search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
                                  "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K, smem_cap));
     c->warps = warps;
@@ -499,7 +499,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     if ((rc2 = alloc(c, reinterpret_cast<void**>(&(ptr)), (bytes), err, errlen)) != PMS8G_OK) \
         return cleanup_fail(rc2);
     AL(c->d_codes, static_cast<size_t>(n) * m);
-    AL(c->d_table, static_cast<size_t>(c->K) * lmer_bytes(c->W));
+    AL(c->d_table, (static_cast<size_t>(c->K) * lmer_bytes(c->W) + 15) / 16 * 16);  // TMA-staged: 16-byte multiple
     AL(c->d_anchors, sizeof(int32_t) * std::max(1, na));
     AL(c->d_l1, sizeof(uint32_t) * static_cast<size_t>(std::max(1, na)) * c->K);
     AL(c->d_meta, sizeof(LevelMeta) * std::max(1, na));
@@ -911,7 +911,7 @@ int scan_setup(ScanBufs& B, const uint8_t* codes, int n, int m, int l, int devic
     *w = m - l + 1;
     const size_t bytes = static_cast<size_t>(n) * m;
     CU(cudaMalloc(&B.codes, bytes));
-    CU(cudaMalloc(&B.table, static_cast<size_t>(n) * *w * lmer_bytes(*W)));
+    CU(cudaMalloc(&B.table, (static_cast<size_t>(n) * *w * lmer_bytes(*W) + 15) / 16 * 16));
     CU(cudaMalloc(&B.flag, sizeof(int)));
     CU(cudaMemsetAsync(B.flag, 0, sizeof(int), B.stream));
     CU(cudaMemcpyAsync(B.codes, codes, bytes, cudaMemcpyHostToDevice, B.stream));

@@ -14,6 +14,41 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// One-dimensional TMA bulk copy global -> shared (cp.async.bulk, completion
+// counted on an mbarrier): used to stage the l-mer table into each CTA's
+// shared memory with one instruction instead of a strided register copy.
+// Call from every thread of the block; `bytes` must be a multiple of 16 and
+// both addresses 16-byte aligned (the table is allocated rounded up).
+__device__ __forceinline__ void tma_stage(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                          unsigned long long* mbar) {
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        // chunks of <= 64 KB (the copy size operand); all complete on one barrier
+        for (uint32_t off = 0; off < bytes; off += 65536u) {
+            const uint32_t n = bytes - off < 65536u ? bytes - off : 65536u;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dst + off),
+                "l"(static_cast<const char*>(gmem_src) + off), "r"(n), "r"(bar)
+                : "memory");
+        }
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar)
+            : "memory");
+    }
+}
+
 template <int W>
 struct Mask {
     uint32_t w[W];

@@ -93,10 +93,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(const Lmer<W>* __restrict__ 
     const int K = n * w;
     const Lmer<W>* table = gtable;
     if (stage) {
-        Lmer<W>* s = reinterpret_cast<Lmer<W>*>(sweep_smem);
-        for (int i = threadIdx.x; i < K; i += blockDim.x) s[i] = gtable[i];
-        __syncthreads();
-        table = s;
+        // TMA bulk copy of the whole table into shared memory
+        __shared__ unsigned long long bar;
+        tma_stage(sweep_smem, gtable, (static_cast<uint32_t>(K) * sizeof(Lmer<W>) + 15u) / 16u * 16u, &bar);
+        table = reinterpret_cast<const Lmer<W>*>(sweep_smem);
     }
     const int lane = threadIdx.x & 31;
     const unsigned long long warps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
@@ -151,7 +151,7 @@ cudaError_t launch_sweep(int W, const void* table, int n, int w, int l, int d, i
                          unsigned long long* keys, unsigned long long* count, long long cap, int sms,
                          cudaStream_t s) {
     if (total == 0) return cudaSuccess;
-    const size_t tbytes = static_cast<size_t>(n) * w * lmer_bytes(W);
+    const size_t tbytes = (static_cast<size_t>(n) * w * lmer_bytes(W) + 15) / 16 * 16;
     int stage = tbytes <= 200 * 1024;
     const size_t smem = stage ? tbytes : 0;
     const int threads = 512;
