@@ -1366,6 +1366,28 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     leaves_out += leaves;
 }
 
+// Root consensus bound: a common neighbour within d of every member exists
+// only if the column costs (members minus the most frequent symbol) sum to at
+// most t*d — NeighborhoodEnumerator::prune's consensus rule at the root
+// (src/neighborhood.cpp:150-154), which fails for every child of the root
+// when it fails here. For 5- and 6-tuples most tuples fail it, and the check
+// costs a few instructions per position instead of building the tables.
+template <int W, int MT>
+__device__ __forceinline__ bool root_consensus_ok(const WarpCtx<W, MT>& C, int t, const Lmer<W>* Tm) {
+    const int lane = C.lane, l = C.P->l;
+    int cost = 0;
+    for (int p = lane; p < l; p += 32) {
+        uint32_t e = 0;  // byte c: members holding symbol c at p
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+            if (i < t) e += 1u << (8 * code_at<W>(Tm[i], p));
+        const uint32_t m2 = __vmaxu4(e, e >> 16);
+        cost += t - static_cast<int>(max(m2 & 0xFFu, (m2 >> 8) & 0xFFu));
+    }
+    cost = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(cost)));
+    return cost <= t * C.P->d;
+}
+
 // Common d-neighbourhood of the t-tuple on the stack + verification. The
 // DFS starts from the root, or (ndon > 0) from ndon donated nodes already
 // copied to the bottom of the node stack.
@@ -1382,6 +1404,13 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
 #pragma unroll
     for (int i = 0; i < MT; ++i)
         if (i < t) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
+    if constexpr (MT >= 5) {
+        if (ndon == 0 && P.prune == 2 && !root_consensus_ok<W, MT>(C, t, Tm)) {
+            C.add(W_TUPLES, 1);
+            C.add(W_CLKP, static_cast<unsigned long long>(clock64() - c0));
+            return;
+        }
+    }
     const bool swar = MT <= 4 && P.d <= 31;
     bool fast = false;
     if constexpr (W == 1 && MT <= 4) fast = swar;
