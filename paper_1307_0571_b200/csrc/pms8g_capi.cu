@@ -311,7 +311,7 @@ int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
     // relatively more per unit of the model (divergent DFS + verification vs
     // bitwise filtering), so t is the smallest depth whose pattern term is at
     // most 10^1.8 x the sample term; fitted on the five BASELINE configs
-    // (13,4)->2, (17,6)->3, (21,8)->3, (23,9)->4 measured on B200.
+    // (13,4)->2, (17,6)->3, (21,8)->3, (23,9)->4, (50,21)->6 measured on B200.
     if (const char* env = std::getenv("PMS8G_THRESHOLD")) {
         const int v = std::atoi(env);
         if (v >= 1) return std::min(v, n);
@@ -332,7 +332,14 @@ int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
         for (int k = 0; k < t; ++k) sum += std::exp(terms[k] - mx);
         const double ls = std::log(static_cast<double>(n)) + std::log(static_cast<double>(l)) + mx + std::log(sum);
         const double lp = terms[t - 1] + log_nd + (t - 1) * log_q + std::log(static_cast<double>(l));
-        if (lp - ls <= beta) return t;
+        if (lp - ls <= beta) {
+            // 5+ member tuples without a common neighbour are rejected by the
+            // root consensus bound before their tables are built, so one level
+            // deeper pays there ((50,21): t=6 31.8 s vs t=5 62.2 s for S1
+            // l-mer 0, 29.0 vs 34.8 s per S1 l-mer over 8)
+            if (t >= 5 && t < MAXT && t < n) ++t;
+            return t;
+        }
     }
     return n;
 }

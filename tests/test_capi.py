@@ -134,3 +134,11 @@ def test_scanner_has_no_cpu_fallback():
         P.brute_force_solve(inst.problem, enumeration_guard=1000)
     with pytest.raises(P.InvalidArgument, match="expected l=8"):
         P.verify_motifs(inst.problem, ["ACGT"])
+
+
+def test_gpu_switch_depth_rule():
+    # host-side model (no device): the GPU-tuned switch depth of the five
+    # BASELINE configs; the reference's own rule gives 2,3,3,3,5
+    cfgs = [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]
+    assert [P.gpu_threshold(20, 600, l, d) for l, d in cfgs] == [2, 3, 3, 4, 6]
+    assert [P.estimate_threshold(20, 600, l, d) for l, d in cfgs] == [2, 3, 3, 3, 5]
