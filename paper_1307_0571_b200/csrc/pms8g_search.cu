@@ -1388,6 +1388,21 @@ __device__ __forceinline__ bool root_consensus_ok(const WarpCtx<W, MT>& C, int t
     return cost <= t * C.P->d;
 }
 
+// The same bound for the m members on the stack (u = stack[m-1] included):
+// they have a common d-neighbour only if their consensus cost is at most m*d,
+// and every deeper member can only add column cost, so a stack that fails it
+// has no motif below it. Checked before the push (which it saves) on levels
+// of 4+ members; Theorem 1 already decides 3-member stacks exactly.
+template <int W, int MT>
+__device__ __forceinline__ bool stack_consensus_ok(const WarpCtx<W, MT>& C, int m) {
+    const WarpFixed& S = *C.S();
+    Lmer<W> Tm[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+        if (i < m) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
+    return root_consensus_ok<W, MT>(C, m, Tm);
+}
+
 // Common d-neighbourhood of the t-tuple on the stack + verification. The
 // DFS starts from the root, or (ndon > 0) from ndon donated nodes already
 // copied to the bottom of the node stack.
@@ -1586,6 +1601,12 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         }
         __syncwarp();
         maybe_donate_dfs<W, MT>(C, kmin, k);
+        if constexpr (MT >= 5) {
+            if (k + 1 >= 4 && P.prune == 2 && !stack_consensus_ok<W, MT>(C, k + 1)) {
+                C.add(W_PUSH, 1);
+                continue;
+            }
+        }
         const bool ok = (k + 1 == t && P.lazy) ? lazy_push<W, MT>(C, k) : filter_push<W, MT>(C, k);
         if (!ok) continue;
         if (k + 1 == t) {
