@@ -1601,7 +1601,7 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         }
         __syncwarp();
         maybe_donate_dfs<W, MT>(C, kmin, k);
-        if constexpr (MT >= 5) {
+        if constexpr (MT >= 4) {
             if (k + 1 >= 4 && P.prune == 2 && !stack_consensus_ok<W, MT>(C, k + 1)) {
                 C.add(W_PUSH, 1);
                 continue;
