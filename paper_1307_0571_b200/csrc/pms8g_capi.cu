@@ -310,8 +310,8 @@ int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
     // (Appendix D, src/solver.cpp:75-117). On the GPU the pattern phase costs
     // relatively more per unit of the model (divergent DFS + verification vs
     // bitwise filtering), so t is the smallest depth whose pattern term is at
-    // most 10^1.8 x the sample term; fitted on the five BASELINE configs
-    // (13,4)->2, (17,6)->3, (21,8)->3, (23,9)->4, (50,21)->6 measured on B200.
+    // most 10^1.3 x the sample term; fitted on the five BASELINE configs
+    // (13,4)->2, (17,6)->3, (21,8)->4, (23,9)->4, (50,21)->6 measured on B200.
     if (const char* env = std::getenv("PMS8G_THRESHOLD")) {
         const int v = std::atoi(env);
         if (v >= 1) return std::min(v, n);
@@ -325,7 +325,7 @@ int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
     const double log_w = std::log(static_cast<double>(m - l + 1));
     std::vector<double> terms;
     for (int k = 1; k <= n; ++k) terms.push_back(k * log_w + 0.5 * k * (k - 1) * log_p);
-    const double beta = 1.8 * std::log(10.0);
+    const double beta = 1.3 * std::log(10.0);
     for (int t = 2; t <= n; ++t) {
         const double mx = *std::max_element(terms.begin(), terms.begin() + t);
         double sum = 0;

@@ -251,7 +251,7 @@ def test_anchor_planted_21_8_and_23_9():
 
 def test_gpu_threshold_rule():
     assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
-        [2, 3, 3, 4, 6]
+        [2, 3, 4, 4, 6]
 
 
 @pytest.mark.parametrize("split", ["static", "queue"])
