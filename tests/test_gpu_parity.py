@@ -242,6 +242,19 @@ def test_branch_planted_50_21():
     assert all(O.is_motif(inst.codes, 50, 21, mo) for mo in got)
 
 
+def test_s1_sample_50_21():
+    # whole S1 l-mers of (50,21) (the planted occurrence's offset in S1 plus
+    # every 50th): the reference needs hours per S1 l-mer, so the checks are
+    # size-independent — the planted motif is found, every motif passes the
+    # CPU oracle's naive scan and the GPU scanner
+    inst = planted(50, 21, 1)
+    anchors = sorted({int(inst.positions[0])} | set(range(0, 551, 50)))
+    got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=anchors))
+    assert inst.motif in got
+    assert all(O.is_motif(inst.codes, 50, 21, mo) for mo in got)
+    assert all(ok for ok, _ in P.verify_motifs(inst.problem, got))
+
+
 def test_anchor_planted_21_8_and_23_9():
     _anchor_parity("anchors_21_8_planted.json", 21, 8)
     _anchor_parity("anchors_23_9_planted.json", 23, 9)
