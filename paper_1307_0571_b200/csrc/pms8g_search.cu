@@ -1218,10 +1218,14 @@ __device__ __forceinline__ bool swar_feasible(uint32_t R, const uint4& T, int pr
     const uint32_t B = R + R24;                              // [03, ...]
     const uint32_t X = __byte_perm(A2, B, 0x0041);           // [13, 03, ., .]
     const uint32_t P2 = __byte_perm(X, S3 + R24, 0x0410);    // [13, 03, 0123, 13]
-    if (prune == 1) return ((P1 + T.x) & (P2 + ((T.y & 0xFFFFu) | 0x80800000u)) & M) == M;
     const uint32_t Y = __byte_perm(A1 + R24, A2 + R24, 0x0040);  // [013, 023, ., .]
     const uint32_t T3 = __byte_perm(S3, Y, 0x5410);              // [012, 123, 013, 023]
-    return ((P1 + T.x) & (P2 + T.y) & (T3 + T.z) & M) == M;
+    // pairs only (prune == 1): the consensus and triple thresholds become
+    // "always pass" (0x80 - 0) instead of a second code path, so no dead
+    // arithmetic is if-converted into the child check
+    const uint32_t ty = prune == 2 ? T.y : ((T.y & 0xFFFFu) | 0x80800000u);
+    const uint32_t tz = prune == 2 ? T.z : M;
+    return ((P1 + T.x) & (P2 + ty) & (T3 + tz) & M) == M;
 }
 
 // Enumeration loop for l <= 32 and t <= 4: nodes are uint4 {h, o, budgets,
