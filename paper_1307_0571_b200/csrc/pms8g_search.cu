@@ -1392,6 +1392,81 @@ __device__ __forceinline__ bool root_consensus_ok(const WarpCtx<W, MT>& C, int t
     return cost <= t * C.P->d;
 }
 
+// Incremental form of the stack consensus bound, used before every push of a
+// 4th+ member: for the k members below level k, G[c] = positions where symbol
+// c is a plurality symbol (count == the column maximum M) and
+// need = (k+1)(l-d) - sum M, computed once per level state; then u passes iff
+// popc(sum over c of G[c] & [u == c]) >= need (adding u raises a column's
+// maximum exactly where u holds a plurality symbol). Kept in the warp's
+// global scratch (L1-resident), 4W+1 words per level.
+template <int W, int MT>
+__device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
+    const SearchParams& P = *C.P;
+    return C.lvl_glob + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap +
+           static_cast<size_t>(P.node_cap) * (sizeof(Node<W>) / 4) + 9 * k;
+}
+
+template <int W, int MT>
+__device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k) {
+    const SearchParams& P = *C.P;
+    const WarpFixed& S = *C.S();
+    const int l = P.l;
+    uint32_t* slot = cons_slot<W, MT>(C, k);
+    int sum_m = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int nb = min(32, l - 32 * w);
+        const uint32_t lm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
+        uint32_t ge[4][MT + 1];  // ge[c][j]: at least j members hold c (j <= k)
+        uint32_t mg[MT + 1];
+#pragma unroll
+        for (int j = 0; j <= MT; ++j) mg[j] = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            ge[c][0] = lm;
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) ge[c][j] = 0u;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                if (i < k) {
+                    const Lmer<W> x = C.T()[S.stack_id[i] & ID_MASK];
+                    const uint32_t e = ((c & 2) ? x.h[w] : ~x.h[w]) & ((c & 1) ? x.o[w] : ~x.o[w]) & lm;
+#pragma unroll
+                    for (int j = MT; j >= 1; --j) ge[c][j] |= ge[c][j - 1] & e;
+                }
+            }
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) mg[j] |= ge[c][j];
+        }
+#pragma unroll
+        for (int j = 1; j <= MT; ++j) sum_m += __popc(mg[j]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t g = 0u;
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
+            if (C.lane == c * W + w) slot[c * W + w] = g;
+        }
+    }
+    if (C.lane == 4 * W) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - sum_m);
+    __syncwarp();
+}
+
+template <int W, int MT>
+__device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint32_t u) {
+    const uint32_t* slot = cons_slot<W, MT>(C, k);
+    const Lmer<W> x = C.T()[u & ID_MASK];
+    int matches = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t h = x.h[w], o = x.o[w];
+        const uint32_t hit = (slot[0 * W + w] & ~h & ~o) | (slot[1 * W + w] & ~h & o) |
+                             (slot[2 * W + w] & h & ~o) | (slot[3 * W + w] & h & o);
+        matches += __popc(hit);
+    }
+    return matches >= static_cast<int>(slot[4 * W]);
+}
+
 // The same bound for the m members on the stack (u = stack[m-1] included):
 // they have a common d-neighbour only if their consensus cost is at most m*d,
 // and every deeper member can only add column cost, so a stack that fails it
@@ -1589,6 +1664,9 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         S.iter_end[kmin] = it1;
     }
     __syncwarp();
+    if constexpr (MT >= 5) {
+        if (kmin >= 3 && P.prune == 2) cons_prepare<W, MT>(C, kmin);
+    }
     int k = kmin;
     while (k >= kmin) {
         const LevelMeta& L = S.lev[k];
@@ -1605,7 +1683,15 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         }
         __syncwarp();
         maybe_donate_dfs<W, MT>(C, kmin, k);
-        if constexpr (MT >= 4) {
+        // stack consensus bound: incremental form in the t >= 5 builds
+        // (checked for most pushes there), direct form in the t = 4 build
+        // (measured faster there: one check per tuple, no per-level tables)
+        if constexpr (MT >= 5) {
+            if (k + 1 >= 4 && P.prune == 2 && !cons_check<W, MT>(C, k, uu)) {
+                C.add(W_PUSH, 1);
+                continue;
+            }
+        } else if constexpr (MT == 4) {
             if (k + 1 >= 4 && P.prune == 2 && !stack_consensus_ok<W, MT>(C, k + 1)) {
                 C.add(W_PUSH, 1);
                 continue;
@@ -1622,6 +1708,9 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
                 S.iter_end[k] = S.lev[k].cnt[S.lev[k].branch];
             }
             __syncwarp();
+            if constexpr (MT >= 5) {
+                if (k >= 3 && P.prune == 2) cons_prepare<W, MT>(C, k);
+            }
         }
     }
 }
