@@ -1096,7 +1096,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.qcap = c->qcap;
         P.qslot_bytes = c->qslot_bytes;
         P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
-        P.don_pushes = 4;
+        P.don_pushes = 32;  // DFS pushes between starvation checks (4: +1.8 % on (17,6), +1.6 % (21,8))
         P.don_rounds_mask = 63;
         P.don_burst = 1;
         if (const char* e = std::getenv("PMS8G_DON_BURST")) P.don_burst = std::max(1, std::atoi(e));
