@@ -13,7 +13,10 @@
  *   pms8g_estimate_threshold <- estimate_threshold include/pms8/solver.hpp:61
  *   pms8g_verify_motifs  <- naive_is_motif src/oracle.cpp:16-37 (`pms8 verify`, tools/pms8.cpp:193-256)
  *   pms8g_brute_force    <- brute_force_solve src/oracle.cpp:65-75
- *   pms8g_queue_*       <- the shared next-job counter of run_parallel src/parallel.cpp:54-60, across GPUs
+ *   pms8g_queue_*        <- the shared next-job counter of run_parallel src/parallel.cpp:54-60, across GPUs
+ *   pms8g_solve_batch    <- several solve() calls of one shape (the paper's 5 seeds per (l,d))
+ *   pms8g_gpu_threshold  <- estimate_threshold re-fitted for the GPU
+ *   pms8g_int_peak       <- (measurement: the roofline's integer-issue denominator)
  *   pms8g_merge_keys     <- canonical_motif_set  include/pms8/solver.hpp:22 (device sort+unique
  *                           of packed motif keys; used after the multi-GPU allgather)
  *
