@@ -78,7 +78,8 @@ typedef struct pms8g_options {
 /* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */
 typedef struct pms8g_report {
     int n, m, l, d, sigma;
-    int threshold;          /* switch depth actually used */
+    int threshold;          /* the reference's switch depth for this call (SolverConfig override, else
+                               estimate_threshold src/solver.cpp:104-117): RunReport::threshold */
     int gpus;               /* devices used by this call (1) */
     int64_t subproblems;    /* S1 l-mers searched by this call */
     int64_t motif_count;    /* unique motifs returned */
@@ -94,6 +95,16 @@ typedef struct pms8g_report {
     int64_t verify_compares; /* candidate x l-mer Hamming compares in verification */
     int64_t enum_nodes;      /* enumeration tree nodes expanded */
     uint64_t device_bytes;   /* device memory held by the context */
+    int device_threshold;    /* switch depth the device search used (GPU-tuned unless overridden;
+                                the motif set does not depend on it) */
+    /* MemoryBreakdown (include/pms8/report.hpp:9-25) of the device layout, in 8-byte words:
+     * pair_matrix_words     level-1 rows of every S1 l-mer (the GPU's replacement of the K x K
+     *                       pair matrix: each anchor's compatible l-mers, row-major)
+     * row_matrix_words      per-warp level buffers (the RowMatrix storage of levels 2..t)
+     * row_bookkeeping_words row tables, task bases/order, work ring, node stacks
+     * packed_words          codes + the bit-plane l-mer table
+     * lookup_table_words    0 (no 2^16 lookup table on the device) */
+    uint64_t pair_matrix_words, row_matrix_words, row_bookkeeping_words, packed_words, lookup_table_words;
 } pms8g_report;
 
 /* Motifs as uppercase strings of length l, concatenated without separators,
@@ -172,6 +183,14 @@ int pms8g_verify_motifs(const uint8_t* codes, int n, int m, int l, int d, const 
  * include/pms8/oracle.hpp:28-29). Independent of the PMS8 tree: an exactness check. */
 int pms8g_brute_force(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, int64_t guard,
                       int device, pms8g_result* out, char* err, size_t errlen);
+
+/* The `pms8 solve --format json` document (tools/pms8.cpp:31-60,171-176) for a result:
+ * {"motifs": [...], "report": {...}} with the reference's report schema, keys in the order
+ * nlohmann::json prints them (sorted), two-space indentation, doubles in shortest round-trip
+ * form. alphabet_name: e.g. "dna"; command: the invocation line. Writes at most cap bytes
+ * (NUL-terminated) and returns the full length (excluding the NUL), or -1 on a NULL result. */
+int64_t pms8g_report_json(const pms8g_result* result, const char* alphabet_name, const char* command, char* out,
+                          size_t cap);
 
 /* Cross-GPU static task queue: one 64-bit claim counter in the HBM of the creating rank's
  * device, mapped into the other ranks' devices over NVLink/NVSwitch with CUDA IPC. Rank 0

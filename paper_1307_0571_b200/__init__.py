@@ -71,8 +71,11 @@ class Alphabet:
     def __init__(self, symbols: str, name: str):
         if len(symbols) < 2:
             raise InvalidArgument(f'alphabet needs at least 2 symbols, got "{symbols}"')
-        if len(set(symbols)) != len(symbols):
-            raise InvalidArgument("duplicate alphabet symbol")
+        seen = set()
+        for ch in symbols:  # Alphabet ctor, src/alphabet.cpp:13-17
+            if ch in seen:
+                raise InvalidArgument(f"duplicate alphabet symbol '{ch}'")
+            seen.add(ch)
         self.symbols = symbols
         self._name = name
         self._lut = np.full(256, 255, np.uint8)
@@ -228,6 +231,8 @@ class RunReport:
     device_bytes: int = 0
     gpus: int = 1
     command: str = ""
+    device_threshold: int = 0
+    memory: dict = dataclasses.field(default_factory=dict)
 
     def fill(self, r: _capi.Report, alphabet_name: str):
         self.n, self.m, self.l, self.d = r.n, r.m, r.l, r.d
@@ -245,6 +250,9 @@ class RunReport:
         self.enum_nodes = r.enum_nodes
         self.device_bytes = r.device_bytes
         self.gpus = r.gpus
+        self.device_threshold = r.device_threshold
+        self.memory = {k: getattr(r, k) for k in ("pair_matrix_words", "row_matrix_words", "row_bookkeeping_words",
+                                                  "packed_words", "lookup_table_words")}
         return self
 
 

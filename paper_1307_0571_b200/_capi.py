@@ -58,6 +58,12 @@ class Report(ctypes.Structure):
         ("verify_compares", ctypes.c_int64),
         ("enum_nodes", ctypes.c_int64),
         ("device_bytes", ctypes.c_uint64),
+        ("device_threshold", ctypes.c_int),
+        ("pair_matrix_words", ctypes.c_uint64),
+        ("row_matrix_words", ctypes.c_uint64),
+        ("row_bookkeeping_words", ctypes.c_uint64),
+        ("packed_words", ctypes.c_uint64),
+        ("lookup_table_words", ctypes.c_uint64),
     ]
 
 
@@ -72,7 +78,7 @@ EXPORTS = [
     "pms8g_ctx_counters",
     "pms8g_ctx_destroy", "pms8g_merge_keys", "pms8g_decode_keys", "pms8g_generate", "pms8g_estimate_threshold",
     "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version", "pms8g_verify_motifs", "pms8g_brute_force",
-    "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy", "pms8g_solve_batch",
+    "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy", "pms8g_solve_batch", "pms8g_report_json",
 ]
 QUEUE_HANDLE_BYTES = 64
 
@@ -145,6 +151,8 @@ def lib():
         L.pms8g_solve_batch.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options),
                                         ctypes.POINTER(Result), c_char_p, c_sz]
         L.pms8g_solve_batch.restype = c_int
+    L.pms8g_report_json.argtypes = [ctypes.POINTER(Result), c_char_p, c_char_p, c_vp, c_sz]
+    L.pms8g_report_json.restype = c_i64
     L.pms8g_version.argtypes = []
     L.pms8g_version.restype = c_char_p
     _lib = L

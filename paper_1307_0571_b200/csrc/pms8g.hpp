@@ -69,8 +69,13 @@ struct RunReport {
     SolveCounters counters;
     int64_t filter_slots = 0, verify_compares = 0, enum_nodes = 0;
     uint64_t device_bytes = 0;
+    int device_threshold = 0;  // switch depth the device search used
     std::string command;
+    pms8g_report raw{};        // the C ABI report (memory breakdown, all counters)
 };
+
+// `pms8 solve --format json` (tools/pms8.cpp:31-60,171-176), byte-identical layout
+std::string report_json(const MotifSet& motifs, const RunReport& report);
 
 MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const GpuOptions& options,
                       RunReport* report = nullptr);
@@ -102,5 +107,9 @@ void write_fasta(const std::string& path, const std::vector<std::string>& names,
 
 // "dna", "custom:<symbols>" -> symbols in code order; throws invalid_argument
 std::string alphabet_symbols(const std::string& name);
+
+// Problem::validate fused with the encoding the device consumes: n*m codes
+// (row-major, 0..sigma-1 in alphabet order); throws invalid_argument.
+std::vector<uint8_t> encode_problem(const Problem& problem);
 
 }  // namespace pms8g

@@ -79,6 +79,7 @@ struct pms8g_queue {
 
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
+    int ref_t = 0;  // the reference's switch depth (override or estimate_threshold), reported
     std::string alphabet;
     pms8g_options opt{};
     std::vector<int32_t> anchors;
@@ -175,6 +176,10 @@ int validate_problem(int n, int m, int l, int d, const char* alphabet, char* err
     if (d < 0 || d > l) return fail(err, errlen, PMS8G_ERR_INVALID, "mismatch budget must be in [0, l], got %d", d);
     const int s = alphabet ? static_cast<int>(std::strlen(alphabet)) : 4;
     if (s < 2) return fail(err, errlen, PMS8G_ERR_INVALID, "alphabet needs at least 2 symbols");
+    for (int i = 0; i < s; ++i)  // Alphabet ctor, src/alphabet.cpp:13-17
+        for (int j = 0; j < i; ++j)
+            if (alphabet[i] == alphabet[j])
+                return fail(err, errlen, PMS8G_ERR_INVALID, "duplicate alphabet symbol '%c'", alphabet[i]);
     // GPU path limits: 2 bit planes, 32 rows per warp table,
     // 24-bit l-mer ids, 16-bit row offsets
     if (s > 4)
@@ -427,6 +432,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     c->w = m - l + 1;
     c->K = n * c->w;
     c->t = t;
+    c->ref_t = opt.threshold > 0 ? opt.threshold : pms8g_estimate_threshold(n, m, l, d, sigma);
     c->opt = opt;
     c->device = dev;
     c->sms = prop.multiProcessorCount;
@@ -621,6 +627,18 @@ void pms8g_decode_keys(const uint64_t* keys, int64_t count, int l, const char* a
             const int code = static_cast<int>(((sh >= 64) ? (hi >> (sh - 64)) : (lo >> sh)) & 3u);
             out[i * l + p] = sym[code];
         }
+    }
+    // keys sort in code order; canonical_motif_set (src/solver.cpp:16-21)
+    // sorts by byte value, which differs when the alphabet's symbols are not
+    // in ascending byte order (e.g. custom:TGCA): re-sort the strings then
+    bool ascending = true;
+    for (const char* q = sym; q[0] && q[1]; ++q)
+        if (static_cast<unsigned char>(q[0]) >= static_cast<unsigned char>(q[1])) ascending = false;
+    if (!ascending && count > 1) {
+        std::vector<std::string> v(static_cast<size_t>(count));
+        for (int64_t i = 0; i < count; ++i) v[static_cast<size_t>(i)].assign(out + i * l, static_cast<size_t>(l));
+        std::sort(v.begin(), v.end());
+        for (int64_t i = 0; i < count; ++i) std::memcpy(out + i * l, v[static_cast<size_t>(i)].data(), l);
     }
 }
 
@@ -866,6 +884,10 @@ int validate_scan(const uint8_t* codes, int n, int m, int l, int d, const char* 
     if (d < 0 || d > l) return fail(err, errlen, PMS8G_ERR_INVALID, "mismatch budget must be in [0, l], got %d", d);
     const int s = alphabet ? static_cast<int>(std::strlen(alphabet)) : 4;
     if (s < 2) return fail(err, errlen, PMS8G_ERR_INVALID, "alphabet needs at least 2 symbols");
+    for (int i = 0; i < s; ++i)  // Alphabet ctor, src/alphabet.cpp:13-17
+        for (int j = 0; j < i; ++j)
+            if (alphabet[i] == alphabet[j])
+                return fail(err, errlen, PMS8G_ERR_INVALID, "duplicate alphabet symbol '%c'", alphabet[i]);
     if (s > 4)
         return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 4 symbols, got %d", s);
     if (l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
@@ -1117,10 +1139,13 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.error_flag = c->d_err;
         P.gqueue = nullptr;
         P.gepoch = 0;
-        if (c->opt.queue) {
+        if (c->opt.queue && attempt == 0) {
             P.gqueue = static_cast<unsigned long long*>(c->opt.queue->dptr);
             P.gepoch = ++c->opt.queue->epoch;
         }
+        // a retry (key buffer grown) searches every task locally: the shared
+        // counter's epoch stays in step with the other ranks, and this rank's
+        // result is a superset of its share (the union is unchanged)
         const char* tl_path = std::getenv("PMS8G_TIMELINE");  // diagnostics: task timeline dump
         unsigned long long* d_tl = nullptr;
         if (tl_path) {
@@ -1129,7 +1154,12 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             P.timeline = d_tl;
         }
         CU(cudaEventRecord(c->ev[2], s));
-        if (na > 0) CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
+        // the dynamic shared-memory limit is a per-kernel attribute, shared by
+        // every context of this (W, t) build in the process: set it per launch
+        if (na > 0) {
+            CU(set_search_smem(c->W, c->t, c->smem));
+            CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
+        }
         CU(cudaEventRecord(c->ev[3], s));
         CU(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long) * C_NCTR, cudaMemcpyDeviceToHost,
                            s));
@@ -1199,7 +1229,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         R.l = c->l;
         R.d = c->d;
         R.sigma = c->sigma;
-        R.threshold = c->t;
+        R.threshold = c->ref_t;
+        R.device_threshold = c->t;
         R.gpus = 1;
         R.subproblems = na;
         R.motif_count = uniq;
@@ -1220,6 +1251,21 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         R.pattern_seconds = ms_search * 1e-3 * frac_pattern;
         R.sample_seconds = R.device_seconds - R.pattern_seconds;
         R.device_bytes = c->device_bytes;
+        {
+            // MemoryBreakdown of the device layout (include/pms8g.h), 8-byte words
+            auto words = [](size_t bytes) { return static_cast<uint64_t>((bytes + 7) / 8); };
+            const size_t nwarps = static_cast<size_t>(c->blocks) * c->warps;
+            const size_t lvl = static_cast<size_t>(std::max(0, c->t - 1)) * c->level_cap * 4 * nwarps;
+            R.pair_matrix_words = words(static_cast<size_t>(std::max(1, na)) * c->K * 4);
+            R.row_matrix_words = words(lvl);
+            R.row_bookkeeping_words =
+                words(sizeof(LevelMeta) * std::max(1, na) + sizeof(long long) * (na + 1) +
+                      sizeof(uint32_t) * 4 * static_cast<size_t>(c->order_cap) +
+                      static_cast<size_t>(c->qcap) * (c->qslot_bytes + sizeof(unsigned int)) +
+                      (c->scratch_words * 4 * nwarps - lvl));
+            R.packed_words = words(static_cast<size_t>(c->n) * c->m + static_cast<size_t>(c->K) * lmer_bytes(c->W));
+            R.lookup_table_words = 0;
+        }
         R.wall_seconds = now_s() - t0;
         return PMS8G_OK;
     }

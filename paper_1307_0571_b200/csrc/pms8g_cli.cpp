@@ -10,7 +10,8 @@
 // stdout/stderr/exit codes follow cmd_solve (tools/pms8.cpp:150-184): one motif
 // per line (or JSON {motifs, report}), a one-line summary on stderr, exit 0 if
 // at least one motif, 1 if none, 2 on usage/input error (:386-389). CLI11 and
-// nlohmann::json are not available here, so argv parsing and JSON are hand-rolled.
+// nlohmann::json are not available here: argv parsing is hand-rolled and the
+// JSON document comes from pms8g_report_json (byte-identical to dump(2)).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,15 +28,6 @@ namespace {
 struct Usage : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
-
-std::string json_escape(const std::string& s) {
-    std::string o;
-    for (char c : s) {
-        if (c == '"' || c == '\\') o += '\\';
-        o += c;
-    }
-    return o;
-}
 
 int to_int(const std::string& flag, const std::string& v) {
     try {
@@ -121,24 +113,7 @@ int cmd_solve(const std::vector<std::string>& args, const std::string& command) 
     const pms8g::MotifSet motifs = pms8g::run_parallel(problem, config, gpu, &report);
     report.command = command;
     if (format == "json") {
-        std::ostringstream o;
-        o << "{\n  \"motifs\": [";
-        for (size_t i = 0; i < motifs.size(); ++i) o << (i ? ", " : "") << "\"" << motifs[i] << "\"";
-        o << "],\n  \"report\": {\"n\": " << report.n << ", \"m\": " << report.m << ", \"l\": " << report.l
-          << ", \"d\": " << report.d << ", \"alphabet\": \"" << json_escape(report.alphabet)
-          << "\", \"threshold\": " << report.threshold << ", \"workers\": " << report.workers
-          << ", \"subproblems\": " << report.subproblems << ", \"motif_count\": " << report.motif_count
-          << ", \"wall_seconds\": " << report.wall_seconds << ", \"sample_seconds\": " << report.sample_seconds
-          << ", \"pattern_seconds\": " << report.pattern_seconds << ", \"device_seconds\": " << report.device_seconds
-          << ", \"memory\": {\"device_bytes\": " << report.device_bytes << "}"
-          << ", \"counters\": {\"stacks_explored\": " << report.counters.stacks_explored
-          << ", \"neighborhoods\": " << report.counters.neighborhoods
-          << ", \"neighbors_visited\": " << report.counters.neighbors_visited
-          << ", \"motifs_emitted\": " << report.counters.motifs_emitted
-          << ", \"filter_slots\": " << report.filter_slots << ", \"verify_compares\": " << report.verify_compares
-          << ", \"enum_nodes\": " << report.enum_nodes << "}, \"command\": \"" << json_escape(report.command)
-          << "\"}\n}";
-        std::cout << o.str() << "\n";
+        std::cout << pms8g::report_json(motifs, report) << "\n";
     } else {
         for (const auto& m : motifs) std::cout << m << "\n";
         std::cerr << "motifs=" << motifs.size() << " threshold=" << report.threshold << " workers=" << report.workers

@@ -1,4 +1,5 @@
-// pms8g_cpp.cpp — C++ host API (pms8g.hpp) over the C ABI, plus FASTA/plain IO.
+// pms8g_cpp.cpp — C++ host API (pms8g.hpp) over the C ABI (sequence files and
+// the problem check live in pms8g_io.cpp).
 #include "pms8g.hpp"
 
 #include <cctype>
@@ -18,86 +19,8 @@ namespace {
     }
 }
 
-std::string slurp(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("cannot open " + path);
-    std::ostringstream ss;
-    ss << in.rdbuf();
-    return ss.str();
-}
-
-std::string strip(const std::string& s) {
-    const size_t b = s.find_first_not_of(" \t\r\n");
-    if (b == std::string::npos) return {};
-    const size_t e = s.find_last_not_of(" \t\r\n");
-    return s.substr(b, e - b + 1);
-}
-
 void upcase(std::string& s) {
     for (char& c : s) c = static_cast<char>(std::toupper(static_cast<unsigned char>(c)));
-}
-
-void parse_comment(const std::string& line, SequenceFile& out) {
-    const std::string body = strip(line.substr(1));
-    const size_t eq = body.find('=');
-    if (eq == std::string::npos || eq == 0) return;
-    out.metadata[strip(body.substr(0, eq))] = strip(body.substr(eq + 1));
-}
-
-// parse_fasta / parse_plain, src/io.cpp:41-95
-SequenceFile parse_fasta(const std::string& text) {
-    SequenceFile out;
-    std::istringstream in(text);
-    std::string line, current;
-    bool have = false;
-    int lineno = 0;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (line.empty()) continue;
-        if (line[0] == ';') {
-            if (!have) parse_comment(line, out);
-            continue;
-        }
-        if (line[0] == '>') {
-            if (have) out.sequences.push_back(std::move(current));
-            current.clear();
-            have = true;
-            out.names.push_back(strip(line.substr(1)));
-            continue;
-        }
-        if (!have)
-            throw std::runtime_error("malformed FASTA: sequence data before any '>' header at line " +
-                                     std::to_string(lineno));
-        std::string chunk = strip(line);
-        upcase(chunk);
-        current += chunk;
-    }
-    if (have) out.sequences.push_back(std::move(current));
-    if (out.sequences.empty()) throw std::runtime_error("malformed FASTA: no records found");
-    for (size_t i = 0; i < out.sequences.size(); ++i)
-        if (out.sequences[i].empty())
-            throw std::runtime_error("malformed FASTA: record " + std::to_string(i + 1) + " (" + out.names[i] +
-                                     ") is empty");
-    return out;
-}
-
-SequenceFile parse_plain(const std::string& text) {
-    SequenceFile out;
-    std::istringstream in(text);
-    std::string line;
-    while (std::getline(in, line)) {
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        std::string s = strip(line);
-        if (s.empty() || s[0] == ';') {
-            if (!s.empty()) parse_comment(s, out);
-            continue;
-        }
-        upcase(s);
-        out.sequences.push_back(std::move(s));
-    }
-    if (out.sequences.empty()) throw std::runtime_error("no sequences found");
-    return out;
 }
 
 }  // namespace
@@ -109,39 +32,20 @@ std::string alphabet_symbols(const std::string& name) {
     if (name.rfind(prefix, 0) == 0) {
         std::string up = name.substr(prefix.size());
         upcase(up);
+        // Alphabet ctor checks, src/alphabet.cpp:10-17
+        if (up.size() < 2) throw std::invalid_argument("alphabet needs at least 2 symbols, got \"" + up + "\"");
+        for (size_t i = 0; i < up.size(); ++i)
+            if (up.find(up[i]) != i)
+                throw std::invalid_argument(std::string("duplicate alphabet symbol '") + up[i] + "'");
         return up;
     }
     throw std::invalid_argument("unknown alphabet \"" + name + "\" (expected dna, protein or custom:<symbols>)");
 }
 
-void Problem::validate() const {
-    if (sequences.empty()) throw std::invalid_argument("no input sequences");
-    const int len = m();
-    if (motif_length < 1) throw std::invalid_argument("motif length must be >= 1");
-    if (motif_length > len)
-        throw std::invalid_argument("motif length " + std::to_string(motif_length) + " exceeds sequence length " +
-                                    std::to_string(len));
-    if (max_mismatches < 0 || max_mismatches > motif_length)
-        throw std::invalid_argument("mismatch budget must be in [0, l], got " + std::to_string(max_mismatches));
-    for (size_t i = 0; i < sequences.size(); ++i) {
-        if (static_cast<int>(sequences[i].size()) != len)
-            throw std::invalid_argument("sequence " + std::to_string(i) + " has length " +
-                                        std::to_string(sequences[i].size()) + ", expected " + std::to_string(len));
-        for (size_t j = 0; j < sequences[i].size(); ++j)
-            if (alphabet.find(sequences[i][j]) == std::string::npos)
-                throw std::invalid_argument("sequence " + std::to_string(i) + ", position " + std::to_string(j) +
-                                            ": symbol '" + sequences[i][j] + "' not in alphabet " + alphabet_name);
-    }
-}
-
 MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const GpuOptions& options,
                       RunReport* report) {
-    problem.validate();
+    const std::vector<uint8_t> codes = encode_problem(problem);  // Problem::validate + codes
     const int n = problem.n(), m = problem.m();
-    std::vector<uint8_t> codes(static_cast<size_t>(n) * m);
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < m; ++j)
-            codes[static_cast<size_t>(i) * m + j] = static_cast<uint8_t>(problem.alphabet.find(problem.sequences[i][j]));
     pms8g_options o;
     pms8g_default_options(&o);
     if (config.threshold_override) {
@@ -187,16 +91,31 @@ MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const 
         report->verify_compares = r.verify_compares;
         report->enum_nodes = r.enum_nodes;
         report->device_bytes = r.device_bytes;
+        report->device_threshold = r.device_threshold;
+        report->raw = r;
     }
     pms8g_result_free(&res);
+    return out;
+}
+
+std::string report_json(const MotifSet& motifs, const RunReport& report) {
+    std::string flat;
+    for (const auto& m : motifs) flat += m;
+    pms8g_result r{};
+    r.count = static_cast<int64_t>(motifs.size());
+    r.l = motifs.empty() ? report.l : static_cast<int>(motifs[0].size());
+    r.motifs = flat.data();
+    r.report = report.raw;
+    const int64_t len = pms8g_report_json(&r, report.alphabet.c_str(), report.command.c_str(), nullptr, 0);
+    std::string out(static_cast<size_t>(len) + 1, '\0');
+    pms8g_report_json(&r, report.alphabet.c_str(), report.command.c_str(), out.data(), out.size());
+    out.resize(static_cast<size_t>(len));
     return out;
 }
 
 MotifSet solve(const Problem& problem, const SolverConfig& config, RunReport* report) {
     return run_parallel(problem, config, GpuOptions{}, report);
 }
-
-SequenceFile read_plain(const std::string& path) { return parse_plain(slurp(path)); }
 
 std::vector<MotifSet> solve_batch(const std::vector<Problem>& problems, const SolverConfig& config, int device) {
     std::vector<MotifSet> out(problems.size());
@@ -205,13 +124,11 @@ std::vector<MotifSet> solve_batch(const std::vector<Problem>& problems, const So
     std::vector<std::vector<uint8_t>> codes;
     std::vector<const uint8_t*> ptrs;
     for (const auto& p : problems) {
-        p.validate();
+        std::vector<uint8_t> c = encode_problem(p);
         if (p.n() != p0.n() || p.m() != p0.m() || p.motif_length != p0.motif_length ||
             p.max_mismatches != p0.max_mismatches || p.alphabet != p0.alphabet)
             throw std::invalid_argument("solve_batch: every problem must have the same n, m, l, d and alphabet");
-        codes.emplace_back();
-        for (const auto& s : p.sequences)
-            for (char ch : s) codes.back().push_back(static_cast<uint8_t>(p.alphabet.find(ch)));
+        codes.push_back(std::move(c));
     }
     for (const auto& c : codes) ptrs.push_back(c.data());
     pms8g_options o;
@@ -244,7 +161,7 @@ std::vector<uint8_t> encode_codes(const std::vector<std::string>& seqs, const st
 }  // namespace
 
 std::vector<MotifCheck> verify_motifs(const Problem& problem, const std::vector<std::string>& motifs, int device) {
-    problem.validate();
+    const std::vector<uint8_t> codes = encode_problem(problem);
     const int n = problem.n(), m = problem.m(), l = problem.motif_length;
     for (const auto& mt : motifs) {
         if (static_cast<int>(mt.size()) != l)
@@ -257,7 +174,6 @@ std::vector<MotifCheck> verify_motifs(const Problem& problem, const std::vector<
     }
     std::vector<MotifCheck> out(motifs.size());
     if (motifs.empty()) return out;
-    const std::vector<uint8_t> codes = encode_codes(problem.sequences, problem.alphabet);
     const std::vector<uint8_t> mc = encode_codes(motifs, problem.alphabet);
     std::vector<int32_t> wit(motifs.size() * n);
     std::vector<uint8_t> pass(motifs.size());
@@ -280,8 +196,7 @@ bool naive_is_motif(const Problem& problem, const std::string& motif, std::vecto
 }
 
 MotifSet brute_force_solve(const Problem& problem, int64_t enumeration_guard, int device) {
-    problem.validate();
-    const std::vector<uint8_t> codes = encode_codes(problem.sequences, problem.alphabet);
+    const std::vector<uint8_t> codes = encode_problem(problem);
     pms8g_result res;
     char err[512] = {0};
     const int rc = pms8g_brute_force(codes.data(), problem.n(), problem.m(), problem.motif_length,
@@ -292,33 +207,6 @@ MotifSet brute_force_solve(const Problem& problem, int64_t enumeration_guard, in
     for (int64_t i = 0; i < res.count; ++i) motifs.emplace_back(res.motifs + i * res.l, res.l);
     pms8g_result_free(&res);
     return motifs;
-}
-
-SequenceFile read_sequences(const std::string& path) {
-    // format sniff, src/io.cpp:101-111
-    const std::string text = slurp(path);
-    std::istringstream in(text);
-    std::string line;
-    while (std::getline(in, line)) {
-        const std::string s = strip(line);
-        if (s.empty() || s[0] == ';') continue;
-        return s[0] == '>' ? parse_fasta(text) : parse_plain(text);
-    }
-    return parse_plain(text);
-}
-
-void write_fasta(const std::string& path, const std::vector<std::string>& names,
-                 const std::vector<std::string>& sequences,
-                 const std::vector<std::pair<std::string, std::string>>& metadata) {
-    std::ofstream out(path, std::ios::binary);
-    if (!out) throw std::runtime_error("cannot write " + path);
-    for (const auto& [k, v] : metadata) out << "; " << k << "=" << v << "\n";
-    constexpr size_t wrap = 70;
-    for (size_t i = 0; i < sequences.size(); ++i) {
-        out << ">" << (i < names.size() ? names[i] : "seq_" + std::to_string(i)) << "\n";
-        for (size_t pos = 0; pos < sequences[i].size(); pos += wrap) out << sequences[i].substr(pos, wrap) << "\n";
-    }
-    if (!out) throw std::runtime_error("write failed for " + path);
 }
 
 }  // namespace pms8g

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "pms8g_common.cuh"
 #include "pms8g_device.cuh"
@@ -2032,8 +2033,21 @@ cudaError_t set_smem_t(size_t bytes) {
 // per-member loop is unrolled over registers; t = 1 runs the MT = 2 build.
 cudaError_t set_search_smem(int W, int t, size_t bytes) {
     const int mt = t < 2 ? 2 : t;
-#define PMS8G_CASE(WW, M) \
-    if (W == WW && mt == M) return set_smem_t<WW, M>(bytes);
+    // the attribute only ever grows (per build and device), so contexts with
+    // smaller plans never lower it under another context's launch
+    static std::mutex mu;
+    static size_t granted[2][MAXT + 1][64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = granted[W - 1][mt][dev & 63];
+    if (bytes <= cur) return cudaSuccess;
+#define PMS8G_CASE(WW, M)                                 \
+    if (W == WW && mt == M) {                             \
+        const cudaError_t e = set_smem_t<WW, M>(bytes);   \
+        if (e == cudaSuccess) cur = bytes;                \
+        return e;                                         \
+    }
     PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
     PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6)
 #undef PMS8G_CASE

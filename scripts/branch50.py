@@ -16,6 +16,6 @@ t0 = time.time()
 got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(branches=br), rep)
 dt = time.time() - t0
 print(f"(50,21) anchor 0 branches 0..{nb-1}: {dt:.2f} s wall, device {rep.device_seconds:.2f} s, motifs {len(got)}, "
-      f"t={rep.threshold} pushes={rep.counters.stacks_explored} tuples={rep.counters.neighborhoods} "
+      f"t={rep.device_threshold} pushes={rep.counters.stacks_explored} tuples={rep.counters.neighborhoods} "
       f"cands={rep.counters.neighbors_visited} slots={rep.filter_slots} vcmp={rep.verify_compares} "
       f"nodes={rep.enum_nodes}", flush=True)

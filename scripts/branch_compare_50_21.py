@@ -42,7 +42,7 @@ print(json.dumps({
     "branches": [list(b) for b in br],
     "reference": {"wall_s": ref_wall, "per_branch_thread_s": ref_secs, "threads": threads,
                   "kind": "reference (oracle/_ref, OpenMP over branches)"},
-    "gpu": {"wall_s": gpu_wall, "device_s": rep.device_seconds, "threshold": rep.threshold,
+    "gpu": {"wall_s": gpu_wall, "device_s": rep.device_seconds, "threshold": rep.device_threshold,
             "pushes": rep.counters.stacks_explored, "tuples": rep.counters.neighborhoods,
             "candidates": rep.counters.neighbors_visited, "verify_compares": rep.verify_compares},
     "speedup_wall": ref_wall / gpu_wall,

@@ -17,5 +17,5 @@ rep = P.RunReport()
 t0 = time.time()
 got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(branches=br), rep)
 print(f"planted branch (50,21): {time.time() - t0:.1f} s, {len(got)} motifs, planted motif found: {motif in got}",
-      f"t={rep.threshold}", flush=True)
+      f"t={rep.device_threshold}", flush=True)
 print(got[:10])

@@ -28,7 +28,7 @@ motifs = ctx.result(rep)
 c = ctx.counters()
 names = ["pushes", "viable", "slots", "tuples", "leaves", "emitted", "vcmp", "nodes", "clk_filter", "clk_pattern",
          "pair_rej", "tri_rej", "tasks", "donated", "replays"]
-print(f"({l},{d}) t={rep.threshold} anchors={rep.subproblems} wall={dt*1e3:.2f}ms search={ctx.kernel_ms()[0]:.2f}ms "
+print(f"({l},{d}) t={rep.device_threshold} anchors={rep.subproblems} wall={dt*1e3:.2f}ms search={ctx.kernel_ms()[0]:.2f}ms "
       f"motifs={motifs}")
 print("  " + " ".join(f"{n}={v}" for n, v in zip(names, c)))
 hist = c[15:55]
@@ -36,7 +36,7 @@ if len(c) > 55:
     import torch
     props = torch.cuda.get_device_properties(0)
     ms = ctx.kernel_ms()[0]
-    warps = 12 if (l <= 32 and rep.threshold <= 3) else 16  # search_default_warps
+    warps = 12 if (l <= 32 and rep.device_threshold <= 3) else 16  # search_default_warps
     tot = props.multi_processor_count * warps * ms * 1e-3 * 1.965e9
     for nm, lo in (("donated ranges", 56), ("donated nodes", 96)):
         print(f"  {nm} histogram: " + " ".join(f"{i}:{v}" for i, v in enumerate(c[lo:lo + 40]) if v))
