@@ -17,6 +17,9 @@
  *   pms8g_solve_batch    <- several solve() calls of one shape (the paper's 5 seeds per (l,d))
  *   pms8g_gpu_threshold  <- estimate_threshold re-fitted for the GPU
  *   pms8g_int_peak       <- (measurement: the roofline's integer-issue denominator)
+ *   pms8g_solve_multi / pms8g_multi_* <- run_parallel over N GPUs (parallel.hpp:37-38,
+ *                           src/parallel.cpp:35-118: GPUs as the worker team)
+ *   pms8g_report_json    <- report_to_json + `--format json` tools/pms8.cpp:31-60,171-176
  *   pms8g_merge_keys     <- canonical_motif_set  include/pms8/solver.hpp:22 (device sort+unique
  *                           of packed motif keys; used after the multi-GPU allgather)
  *
@@ -151,6 +154,8 @@ int pms8g_ctx_result(pms8g_ctx* ctx, pms8g_result* out, char* err, size_t errlen
 void* pms8g_ctx_stream(pms8g_ctx* ctx); /* cudaStream_t */
 /* Dedicated event pair around the main search kernel of the last launch. */
 int pms8g_ctx_kernel_ms(pms8g_ctx* ctx, float* search_ms, float* rowbuild_ms);
+/* Report of the last run (owned by the context, valid until the next run). */
+int pms8g_ctx_report(pms8g_ctx* ctx, const pms8g_report** report);
 /* Raw device counters of the last run (diagnostics: per-rule rejections, task
  * duration histogram); returns the number of counters available. */
 int pms8g_ctx_counters(pms8g_ctx* ctx, uint64_t* out, int cap);
@@ -191,6 +196,26 @@ int pms8g_brute_force(const uint8_t* codes, int n, int m, int l, int d, const ch
  * (NUL-terminated) and returns the full length (excluding the NUL), or -1 on a NULL result. */
 int64_t pms8g_report_json(const pms8g_result* result, const char* alphabet_name, const char* command, char* out,
                           size_t cap);
+
+/* run_parallel over several GPUs in one blocking call (include/pms8/parallel.hpp:37-38 with
+ * GPUs as the workers): one host thread and device context per entry of `devices`; all
+ * contexts search every S1 l-mer, claiming (S1 l-mer, depth-1 branch) tasks from one counter
+ * in devices[0]'s HBM over NVLink peer access (static split offset % N == rank when a device
+ * cannot reach it); the per-device motif sets are unioned with ncclAllGather (distinct devices,
+ * NCCL loadable) or peer copies, then sorted and deduplicated on devices[0]. The result and
+ * report cover the whole run (report.gpus = ndevices, counters summed). A device may be listed
+ * more than once (several contexts share it: the one-GPU test hook). opt.queue, opt.shard_*
+ * and opt.branches must be unset. pms8g_solve_multi caches one handle per process. */
+typedef struct pms8g_multi pms8g_multi;
+int pms8g_multi_create(int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt,
+                       const int* devices, int ndevices, pms8g_multi** out, char* err, size_t errlen);
+/* codes: HOST n*m codes; blocking. */
+int pms8g_multi_run(pms8g_multi* h, const uint8_t* codes, pms8g_result* out, char* err, size_t errlen);
+/* "nccl-allgather" or "peer-copy": how the motif sets are exchanged. */
+const char* pms8g_multi_exchange(const pms8g_multi* h);
+void pms8g_multi_destroy(pms8g_multi* h);
+int pms8g_solve_multi(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt,
+                      const int* devices, int ndevices, pms8g_result* out, char* err, size_t errlen);
 
 /* Cross-GPU static task queue: one 64-bit claim counter in the HBM of the creating rank's
  * device, mapped into the other ranks' devices over NVLink/NVSwitch with CUDA IPC. Rank 0

@@ -21,6 +21,7 @@
 //   time   l d seed threads stride [t]     -> ctx build + strided anchors, timing JSON
 //   branch l d seed anchor "i1,i2,.." [t]  -> motif set of depth-1 branches (anchor, row[i])
 //   stats  l d seed "o1,.." [t]            -> per-depth work counters (mirrors recurse())
+//   branchtime l d seed threads jobs cap [t] -> capped depth-1 branch sample (CPU baseline, (50,21))
 //   kat                                    -> SPEC known-answer values as JSON
 //   file   path l d threads [t]            -> solve sequences read from a file (one per line)
 #include <omp.h>
@@ -356,6 +357,129 @@ int cmd_branch(int argc, char** argv) {
     return 0;
 }
 
+// recurse (src/solver.cpp:406-419) through the public push/pop/rows API like
+// stats_recurse, giving up once `deadline` passes (the subtree is then only
+// partly searched: its time is a lower bound). Returns false on timeout.
+bool timed_recurse(const SolverContext& ctx, MotifSearch& s, double deadline, std::vector<std::string>& out) {
+    const int p = s.depth();
+    const auto& rows = s.rows();
+    const auto live = rows.live(rows.row_at_position(p));
+    std::vector<uint32_t> snap(live.begin(), live.end());
+    for (uint32_t u : snap) {
+        if (now() > deadline) return false;
+        bool ok = true;
+        if (s.push(u)) {
+            auto& rw = const_cast<RowMatrix&>(s.rows());
+            rw.sort_rows_by_size(s.depth());
+            if (s.depth() == ctx.threshold()) s.enumerate_and_collect(out);
+            else ok = timed_recurse(ctx, s, deadline, out);
+        }
+        s.pop();
+        if (!ok) return false;
+    }
+    return true;
+}
+
+// Bounded CPU sample for configs where one S1 l-mer exceeds any budget
+// ((50,21)): `jobs` depth-1 branches spread over the S1
+// l-mers (anchor = i * w / jobs, branch index = a fixed hash of i modulo the
+// anchor's branching-row size), run in an OpenMP dynamic loop, each capped
+// at cap_seconds. Also counts every S1 l-mer's depth-1 branches (the
+// projection's multiplier). Output: one BTIME line per job, then SUMMARY.
+int cmd_branchtime(int argc, char** argv) {
+    const int l = std::atoi(argv[2]), d = std::atoi(argv[3]);
+    const uint64_t seed = std::strtoull(argv[4], nullptr, 10);
+    const int threads = std::atoi(argv[5]);
+    const int jobs = std::atoi(argv[6]);
+    const double cap = std::atof(argv[7]);
+    const int t = argc > 8 ? std::atoi(argv[8]) : 0;
+    const auto inst = make(l, d, seed);
+    const double t0 = now();
+    SolverContext ctx(inst.problem, config_with(t));
+    const double t1 = now();
+    const auto& set = ctx.set();
+    const int w = inst.problem.m() - l + 1;
+    // depth-1 branch rows of every S1 l-mer (run_anchored's setup, src/solver.cpp:427-432)
+    std::vector<std::vector<uint32_t>> brow(static_cast<size_t>(w));
+    std::atomic<long> next{0};
+#pragma omp parallel num_threads(threads)
+    {
+        MotifSearch s(ctx);
+        for (;;) {
+            const long a = next.fetch_add(1);
+            if (a >= w) break;
+            auto& rw = const_cast<RowMatrix&>(s.rows());
+            rw.reset_full();
+            rw.restrict_row(0, set.lmer_id(0, static_cast<uint32_t>(a)));
+            rw.sort_rows_by_size(0);
+            if (s.push(set.lmer_id(0, static_cast<uint32_t>(a)))) {
+                rw.sort_rows_by_size(1);
+                const auto live = s.rows().live(s.rows().row_at_position(1));
+                brow[static_cast<size_t>(a)].assign(live.begin(), live.end());
+            }
+            s.pop();
+        }
+    }
+    long long total_branches = 0;
+    for (const auto& b : brow) total_branches += static_cast<long long>(b.size());
+    const double t2 = now();
+    std::vector<long> ja(static_cast<size_t>(jobs)), jb(static_cast<size_t>(jobs));
+    for (int i = 0; i < jobs; ++i) {
+        long a = static_cast<long>(i) * w / jobs;
+        while (brow[static_cast<size_t>(a)].empty()) a = (a + 1) % w;
+        ja[static_cast<size_t>(i)] = a;
+        const unsigned long long h = (static_cast<unsigned long long>(i) + 1) * 0x9E3779B97F4A7C15ull;
+        jb[static_cast<size_t>(i)] = static_cast<long>((h >> 33) % brow[static_cast<size_t>(a)].size());
+    }
+    std::vector<double> secs(static_cast<size_t>(jobs));
+    std::vector<int> done(static_cast<size_t>(jobs));
+    std::vector<size_t> nmot(static_cast<size_t>(jobs));
+    next = 0;
+#pragma omp parallel num_threads(threads)
+    {
+        MotifSearch s(ctx);
+        for (;;) {
+            const long j = next.fetch_add(1);
+            if (j >= jobs) break;
+            const long a = ja[static_cast<size_t>(j)];
+            const double b0 = now();
+            std::vector<std::string> out;
+            bool complete = true;
+            auto& rw = const_cast<RowMatrix&>(s.rows());
+            rw.reset_full();
+            rw.restrict_row(0, set.lmer_id(0, static_cast<uint32_t>(a)));
+            rw.sort_rows_by_size(0);
+            if (s.push(set.lmer_id(0, static_cast<uint32_t>(a)))) {
+                rw.sort_rows_by_size(1);
+                if (s.push(brow[static_cast<size_t>(a)][static_cast<size_t>(jb[static_cast<size_t>(j)])])) {
+                    rw.sort_rows_by_size(2);
+                    if (s.depth() == ctx.threshold()) s.enumerate_and_collect(out);
+                    else complete = timed_recurse(ctx, s, b0 + cap, out);
+                }
+                s.pop();
+            }
+            s.pop();
+            secs[static_cast<size_t>(j)] = now() - b0;
+            done[static_cast<size_t>(j)] = complete ? 1 : 0;
+            nmot[static_cast<size_t>(j)] = canonical_motif_set(out).size();
+        }
+    }
+    const double t3 = now();
+    double sum = 0;
+    int ndone = 0;
+    for (int j = 0; j < jobs; ++j) {
+        sum += secs[static_cast<size_t>(j)];
+        ndone += done[static_cast<size_t>(j)];
+        std::printf("BTIME %ld %ld %.6f %d %zu\n", ja[static_cast<size_t>(j)], jb[static_cast<size_t>(j)],
+                    secs[static_cast<size_t>(j)], done[static_cast<size_t>(j)], nmot[static_cast<size_t>(j)]);
+    }
+    std::printf("SUMMARY {\"ctx_seconds\": %.6f, \"branchrow_seconds\": %.6f, \"sample_seconds\": %.6f, "
+                "\"jobs\": %d, \"completed\": %d, \"cap_seconds\": %.3f, \"thread_seconds\": %.6f, "
+                "\"total_branches\": %lld, \"s1_lmers\": %d, \"threads\": %d, \"threshold\": %d}\n",
+                t1 - t0, t2 - t1, t3 - t2, jobs, ndone, cap, sum, total_branches, w, threads, ctx.threshold());
+    return 0;
+}
+
 int cmd_stats(int argc, char** argv) {
     const int l = std::atoi(argv[2]), d = std::atoi(argv[3]);
     const uint64_t seed = std::strtoull(argv[4], nullptr, 10);
@@ -525,6 +649,7 @@ int main(int argc, char** argv) {
         if (cmd == "time" && argc >= 7) return cmd_time(argc, argv);
         if (cmd == "branch" && argc >= 7) return cmd_branch(argc, argv);
         if (cmd == "stats" && argc >= 6) return cmd_stats(argc, argv);
+        if (cmd == "branchtime" && argc >= 8) return cmd_branchtime(argc, argv);
         if (cmd == "kat") return cmd_kat();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());

@@ -198,6 +198,7 @@ class ParallelOptions:
     branches: Optional[Sequence] = None  # explicit depth-1 branches [(s1_offset, seq, offset), ...]
     queue: Optional[object] = None  # parallel.SharedQueue: cross-GPU dynamic pull (exclusive with shard_count > 1)
     split: str = "queue"  # run_parallel under torch.distributed: "queue" (shared cross-GPU queue) or "static"
+    devices: Optional[Sequence[int]] = None  # one process, several GPUs (pms8g_solve_multi): the worker team
 
 
 @dataclasses.dataclass
@@ -313,8 +314,14 @@ def _solve_codes(codes: np.ndarray, l: int, d: int, alphabet: Alphabet, config, 
         return []
     res = _capi.Result()
     err = ctypes.create_string_buffer(512)
-    rc = L.pms8g_solve(codes.ctypes.data, n, m, l, d, alphabet.symbols.encode(), ctypes.byref(o), ctypes.byref(res),
-                       err, len(err))
+    if par is not None and par.devices is not None:
+        devs = np.ascontiguousarray(np.asarray(list(par.devices), np.int32))
+        o.device = -1
+        rc = L.pms8g_solve_multi(codes.ctypes.data, n, m, l, d, alphabet.symbols.encode(), ctypes.byref(o),
+                                 devs.ctypes.data, len(devs), ctypes.byref(res), err, len(err))
+    else:
+        rc = L.pms8g_solve(codes.ctypes.data, n, m, l, d, alphabet.symbols.encode(), ctypes.byref(o),
+                           ctypes.byref(res), err, len(err))
     del keep
     if rc != 0:
         _raise(rc, err)

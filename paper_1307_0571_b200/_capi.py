@@ -79,6 +79,8 @@ EXPORTS = [
     "pms8g_ctx_destroy", "pms8g_merge_keys", "pms8g_decode_keys", "pms8g_generate", "pms8g_estimate_threshold",
     "pms8g_gpu_threshold", "pms8g_int_peak", "pms8g_version", "pms8g_verify_motifs", "pms8g_brute_force",
     "pms8g_queue_create", "pms8g_queue_open", "pms8g_queue_destroy", "pms8g_solve_batch", "pms8g_report_json",
+    "pms8g_ctx_report", "pms8g_multi_create", "pms8g_multi_run", "pms8g_multi_exchange", "pms8g_multi_destroy",
+    "pms8g_solve_multi",
 ]
 QUEUE_HANDLE_BYTES = 64
 
@@ -153,6 +155,20 @@ def lib():
         L.pms8g_solve_batch.restype = c_int
     L.pms8g_report_json.argtypes = [ctypes.POINTER(Result), c_char_p, c_char_p, c_vp, c_sz]
     L.pms8g_report_json.restype = c_i64
+    L.pms8g_ctx_report.argtypes = [c_vp, ctypes.POINTER(ctypes.POINTER(Report))]
+    L.pms8g_ctx_report.restype = c_int
+    L.pms8g_multi_create.argtypes = [c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options), c_vp, c_int,
+                                     ctypes.POINTER(c_vp), c_char_p, c_sz]
+    L.pms8g_multi_create.restype = c_int
+    L.pms8g_multi_run.argtypes = [c_vp, c_vp, ctypes.POINTER(Result), c_char_p, c_sz]
+    L.pms8g_multi_run.restype = c_int
+    L.pms8g_multi_exchange.argtypes = [c_vp]
+    L.pms8g_multi_exchange.restype = c_char_p
+    L.pms8g_multi_destroy.argtypes = [c_vp]
+    L.pms8g_multi_destroy.restype = None
+    L.pms8g_solve_multi.argtypes = [c_vp, c_int, c_int, c_int, c_int, c_char_p, ctypes.POINTER(Options), c_vp, c_int,
+                                    ctypes.POINTER(Result), c_char_p, c_sz]
+    L.pms8g_solve_multi.restype = c_int
     L.pms8g_version.argtypes = []
     L.pms8g_version.restype = c_char_p
     _lib = L

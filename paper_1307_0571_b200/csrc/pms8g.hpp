@@ -53,6 +53,9 @@ struct GpuOptions {
     int device = -1;
     int shard_rank = 0, shard_count = 1;
     std::vector<int32_t> anchors;  // empty: all S1 offsets
+    // several GPUs of this process as the worker team (pms8g_solve_multi):
+    // shared task counter over NVLink, NCCL allgather of the motif sets
+    std::vector<int> devices;
 };
 
 struct SolveCounters {

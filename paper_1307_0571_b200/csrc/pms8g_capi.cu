@@ -25,6 +25,7 @@
 
 #include "../../include/pms8g.h"
 #include "pms8g_device.cuh"
+#include "pms8g_internal.h"
 #include "pms8g_launch.h"
 
 using namespace pms8g;
@@ -36,23 +37,7 @@ struct Err {
     std::string msg;
 };
 
-int fail(char* err, size_t errlen, int code, const char* fmt, ...) {
-    if (err && errlen) {
-        va_list ap;
-        va_start(ap, fmt);
-        std::vsnprintf(err, errlen, fmt, ap);
-        va_end(ap);
-    }
-    return code;
-}
-
-#define CU(call)                                                                                               \
-    do {                                                                                                       \
-        cudaError_t e__ = (call);                                                                              \
-        if (e__ != cudaSuccess)                                                                                \
-            return fail(err, errlen, PMS8G_ERR_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorName(e__), \
-                        __FILE__, __LINE__, cudaGetErrorString(e__));                                          \
-    } while (0)
+#define CU(call) PMS8G_CU(call)
 
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -69,13 +54,6 @@ unsigned __int128 nsize(int l, int d, int sigma) {
 }
 
 }  // namespace
-
-struct pms8g_queue {
-    void* dptr = nullptr;       // the shared counter, mapped on this rank's device
-    int device = 0;
-    int owner = 0;              // 1: allocated here (cudaFree), 0: IPC-opened (cudaIpcCloseMemHandle)
-    unsigned long long epoch = 0;  // runs issued through this queue by this rank
-};
 
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
@@ -130,6 +108,60 @@ struct pms8g_ctx {
     long long unique_count = 0;
     pms8g_report report{};
 };
+
+namespace pms8g {
+
+int merge_keys_with(MergeScratch& m, const void* dev_in, long long count, void* dev_out, long long* out_count,
+                    cudaStream_t s, char* err, size_t errlen) {
+    using K128 = unsigned __int128;
+    *out_count = 0;
+    if (count <= 0) return PMS8G_OK;
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    if (m.device != dev) {
+        merge_scratch_free(m);
+        m.device = dev;
+    }
+    if (count > m.cap) {
+        const long long cap = std::max<long long>(count, 2 * m.cap);
+        if (m.sorted) cudaFree(m.sorted);
+        if (m.temp) cudaFree(m.temp);
+        m.sorted = m.temp = nullptr;
+        m.cap = 0;
+        size_t b1 = 0, b2 = 0;
+        CU(cudaMalloc(&m.sorted, sizeof(K128) * cap));
+        if (!m.count) CU(cudaMalloc(&m.count, sizeof(long long)));
+        if (!m.h_count) CU(cudaMallocHost(&m.h_count, sizeof(long long)));
+        cub::DeviceRadixSort::SortKeys(nullptr, b1, static_cast<const K128*>(nullptr), static_cast<K128*>(nullptr),
+                                       static_cast<int>(cap), 0, 128, s);
+        cub::DeviceSelect::Unique(nullptr, b2, static_cast<const K128*>(nullptr), static_cast<K128*>(nullptr),
+                                  m.count, static_cast<int>(cap), s);
+        m.temp_bytes = std::max(b1, b2);
+        CU(cudaMalloc(&m.temp, m.temp_bytes));
+        m.cap = cap;
+    }
+    size_t bytes = m.temp_bytes;
+    CU(cub::DeviceRadixSort::SortKeys(m.temp, bytes, static_cast<const K128*>(dev_in), static_cast<K128*>(m.sorted),
+                                      static_cast<int>(count), 0, 128, s));
+    bytes = m.temp_bytes;
+    CU(cub::DeviceSelect::Unique(m.temp, bytes, static_cast<const K128*>(m.sorted), static_cast<K128*>(dev_out),
+                                 m.count, static_cast<int>(count), s));
+    CU(cudaMemcpyAsync(m.h_count, m.count, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *out_count = *m.h_count;
+    return PMS8G_OK;
+}
+
+void merge_scratch_free(MergeScratch& m) {
+    if (m.device >= 0) cudaSetDevice(m.device);
+    if (m.sorted) cudaFree(m.sorted);
+    if (m.temp) cudaFree(m.temp);
+    if (m.count) cudaFree(m.count);
+    if (m.h_count) cudaFreeHost(m.h_count);
+    m = MergeScratch{};
+}
+
+}  // namespace pms8g
 
 namespace {
 
@@ -275,8 +307,8 @@ int pms8g_queue_open(const uint8_t* handle, int device, pms8g_queue** out, char*
 void pms8g_queue_destroy(pms8g_queue* q) {
     if (!q) return;
     cudaSetDevice(q->device);
-    if (q->owner) cudaFree(q->dptr);
-    else cudaIpcCloseMemHandle(q->dptr);
+    if (q->owner == 1) cudaFree(q->dptr);
+    else if (q->owner == 0) cudaIpcCloseMemHandle(q->dptr);
     delete q;
 }
 
@@ -603,6 +635,11 @@ int pms8g_ctx_keys(pms8g_ctx* c, const uint64_t** dev_keys, int64_t* count) {
     return PMS8G_OK;
 }
 
+int pms8g_ctx_report(pms8g_ctx* c, const pms8g_report** out) {
+    *out = &c->report;
+    return PMS8G_OK;
+}
+
 int pms8g_ctx_counters(pms8g_ctx* c, uint64_t* out, int cap) {
     const int k = cap < C_NCTR ? cap : C_NCTR;
     for (int i = 0; i < k; ++i) out[i] = c->h_counters[i];
@@ -670,34 +707,19 @@ void pms8g_result_free(pms8g_result* r) {
 
 int pms8g_merge_keys(const uint64_t* dev_in, int64_t count, uint64_t* dev_out, int64_t* out_count, void* stream,
                      char* err, size_t errlen) {
-    using K128 = unsigned __int128;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // one grow-only scratch per device (allocated once, reused by every merge)
+    static std::mutex mu;
+    static MergeScratch scratch[64];
     *out_count = 0;
     if (count <= 0) return PMS8G_OK;
-    K128* tmp = nullptr;
-    long long* d_n = nullptr;
-    void* temp = nullptr;
-    size_t b1 = 0, b2 = 0;
-    CU(cudaMalloc(&tmp, sizeof(K128) * count));
-    CU(cudaMalloc(&d_n, sizeof(long long)));
-    cub::DeviceRadixSort::SortKeys(nullptr, b1, reinterpret_cast<const K128*>(dev_in), tmp, static_cast<int>(count),
-                                   0, 128, s);
-    cub::DeviceSelect::Unique(nullptr, b2, tmp, reinterpret_cast<K128*>(dev_out), d_n, static_cast<int>(count), s);
-    CU(cudaMalloc(&temp, std::max(b1, b2)));
-    size_t bytes = std::max(b1, b2);
-    CU(cub::DeviceRadixSort::SortKeys(temp, bytes, reinterpret_cast<const K128*>(dev_in), tmp,
-                                      static_cast<int>(count), 0, 128, s));
-    bytes = std::max(b1, b2);
-    CU(cub::DeviceSelect::Unique(temp, bytes, tmp, reinterpret_cast<K128*>(dev_out), d_n, static_cast<int>(count),
-                                 s));
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
     long long n = 0;
-    CU(cudaMemcpyAsync(&n, d_n, sizeof n, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    cudaFree(tmp);
-    cudaFree(d_n);
-    cudaFree(temp);
+    const int rc = merge_keys_with(scratch[dev & 63], dev_in, count, dev_out, &n, static_cast<cudaStream_t>(stream),
+                                   err, errlen);
     *out_count = n;
-    return PMS8G_OK;
+    return rc;
 }
 
 namespace {

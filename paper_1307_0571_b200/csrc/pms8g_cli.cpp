@@ -3,6 +3,7 @@
 //   pms8g solve <input> [-l L] [-d D] [--alphabet A] [--workers N] [--threshold T]
 //               [--max-motifs K] [--format text|json] [--prune none|pairs|full]
 //               [--no-sort-rows] [--no-pair-matrix] [--reverify] [--device N]
+//               [--gpus N | --devices a,b,...]   (several GPUs: pms8g_solve_multi)
 //   pms8g verify <input> -M MOTIFS [-l L] [-d D] [--alphabet A] [--device N]
 //   pms8g generate -l L -d D [-n N] [-m M] [--alphabet A] [--seed S]
 //               [--mutation atmost|exact] [-o FILE]
@@ -46,6 +47,7 @@ int cmd_solve(const std::vector<std::string>& args, const std::string& command) 
     std::optional<int64_t> max_motifs;
     bool no_sort = false, no_pair = false, reverify = false;
     int device = -1;
+    std::vector<int> devices;  // --gpus N / --devices a,b: one process, N GPUs
     for (size_t i = 0; i < args.size(); ++i) {
         const std::string& a = args[i];
         auto val = [&]() -> std::string {
@@ -68,7 +70,18 @@ int cmd_solve(const std::vector<std::string>& args, const std::string& command) 
         else if (a == "--no-pair-matrix") no_pair = true;
         else if (a == "--reverify") reverify = true;
         else if (a == "--device") device = to_int(a, val());
-        else if (!a.empty() && a[0] == '-') throw Usage("unknown option " + a);
+        else if (a == "--gpus") {
+            const int g = to_int(a, val());
+            if (g < 1) throw Usage("--gpus: at least 1");
+            devices.clear();
+            for (int i = 0; i < g; ++i) devices.push_back(i);
+        } else if (a == "--devices") {
+            devices.clear();
+            std::string list = val(), tok;
+            std::istringstream ls(list);
+            while (std::getline(ls, tok, ',')) devices.push_back(to_int(a, tok));
+            if (devices.empty()) throw Usage("--devices: a comma-separated list of GPU ordinals");
+        } else if (!a.empty() && a[0] == '-') throw Usage("unknown option " + a);
         else if (input.empty()) input = a;
         else throw Usage("unexpected argument " + a);
     }
@@ -109,6 +122,8 @@ int cmd_solve(const std::vector<std::string>& args, const std::string& command) 
                                             : pms8g::PruneLevel::full;
     pms8g::GpuOptions gpu;
     gpu.device = device;
+    if (devices.size() > 1) gpu.devices = devices;
+    else if (devices.size() == 1) gpu.device = devices[0];
     pms8g::RunReport report;
     const pms8g::MotifSet motifs = pms8g::run_parallel(problem, config, gpu, &report);
     report.command = command;

@@ -65,8 +65,13 @@ MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const 
     }
     pms8g_result res;
     char err[512] = {0};
-    const int rc = pms8g_solve(codes.data(), n, m, problem.motif_length, problem.max_mismatches,
-                               problem.alphabet.c_str(), &o, &res, err, sizeof err);
+    const int rc =
+        options.devices.empty()
+            ? pms8g_solve(codes.data(), n, m, problem.motif_length, problem.max_mismatches, problem.alphabet.c_str(),
+                          &o, &res, err, sizeof err)
+            : pms8g_solve_multi(codes.data(), n, m, problem.motif_length, problem.max_mismatches,
+                                problem.alphabet.c_str(), &o, options.devices.data(),
+                                static_cast<int>(options.devices.size()), &res, err, sizeof err);
     if (rc != PMS8G_OK) rethrow(rc, err);
     MotifSet out;
     out.reserve(static_cast<size_t>(res.count));

@@ -56,6 +56,11 @@ struct WarpFixed {
     unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
     uint32_t lazy_mask;          // rows of the lazy level already filtered
     int lazy_level;              // level whose rows are filtered on demand (0: none)
+    // consensus prefilter of the branching row (levels whose push adds a 4th+
+    // member): bit i = entry cbase[k] + i passed cons_check, for 32 entries
+    // evaluated lane-parallel at once; cbase < 0: nothing cached
+    uint32_t cmask[MAXT + 1];
+    int32_t cbase[MAXT + 1];
 };
 
 enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
@@ -1468,6 +1473,44 @@ __device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint3
     return matches >= static_cast<int>(slot[4 * W]);
 }
 
+// Next branching-row index >= it (and < end) of level k whose l-mer passes the
+// stack consensus bound, or end. The bound is evaluated for 32 consecutive
+// entries at once (one lane each) and cached as a mask, so a warp no longer
+// spends a whole loop iteration on every candidate the bound rejects (most of
+// them at t >= 5). Skipped candidates count as pushes (they are tree nodes).
+template <int W, int MT>
+__device__ __forceinline__ int next_consensus_candidate(WarpCtx<W, MT>& C, int k, int it, int end) {
+    WarpFixed& S = *C.S();
+    const LevelMeta& L = S.lev[k];
+    const uint32_t* row = level_entries<W, MT>(C, k) + L.start[L.branch];
+    const int it0 = it;
+    while (it < end) {
+        int base = S.cbase[k];
+        uint32_t mask = S.cmask[k];
+        if (base < 0 || it < base || it >= base + 32) {
+            base = it;
+            const int e = base + C.lane;
+            const bool pass = e < end && cons_check<W, MT>(C, k, row[e]);
+            mask = __ballot_sync(0xffffffffu, pass);
+            __syncwarp();
+            if (C.lane == 0) {
+                S.cbase[k] = base;
+                S.cmask[k] = mask;
+            }
+            __syncwarp();
+        }
+        const uint32_t m = mask >> (it - base);
+        if (m) {
+            it += __ffs(m) - 1;
+            break;
+        }
+        it = base + 32;
+    }
+    if (it > end) it = end;
+    C.add(W_PUSH, static_cast<unsigned long long>(it - it0));
+    return it;
+}
+
 // The same bound for the m members on the stack (u = stack[m-1] included):
 // they have a common d-neighbour only if their consensus cost is at most m*d,
 // and every deeper member can only add column cost, so a stack that fails it
@@ -1665,14 +1708,24 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         S.iter_end[kmin] = it1;
     }
     __syncwarp();
-    if constexpr (MT >= 5) {
+    // stack consensus bound (t >= 4 builds, pushes of a 4th+ member): the
+    // level's plurality masks are prepared once per level state (cons_prepare)
+    // and the branching row is screened 32 entries at a time
+    constexpr bool kCons = MT >= 4;
+    if constexpr (kCons) {
+        if (C.lane == 0) S.cbase[kmin] = -1;
+        __syncwarp();
         if (kmin >= 3 && P.prune == 2) cons_prepare<W, MT>(C, kmin);
     }
     int k = kmin;
     while (k >= kmin) {
         const LevelMeta& L = S.lev[k];
-        const int it = S.iter[k];
-        if (it >= S.iter_end[k]) {
+        int it = S.iter[k];
+        const int end = S.iter_end[k];
+        if constexpr (kCons) {
+            if (k >= 3 && P.prune == 2 && it < end) it = next_consensus_candidate<W, MT>(C, k, it, end);
+        }
+        if (it >= end) {
             --k;
             continue;
         }
@@ -1684,20 +1737,6 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         }
         __syncwarp();
         maybe_donate_dfs<W, MT>(C, kmin, k);
-        // stack consensus bound: incremental form in the t >= 5 builds
-        // (checked for most pushes there), direct form in the t = 4 build
-        // (measured faster there: one check per tuple, no per-level tables)
-        if constexpr (MT >= 5) {
-            if (k + 1 >= 4 && P.prune == 2 && !cons_check<W, MT>(C, k, uu)) {
-                C.add(W_PUSH, 1);
-                continue;
-            }
-        } else if constexpr (MT == 4) {
-            if (k + 1 >= 4 && P.prune == 2 && !stack_consensus_ok<W, MT>(C, k + 1)) {
-                C.add(W_PUSH, 1);
-                continue;
-            }
-        }
         const bool ok = (k + 1 == t && P.lazy) ? lazy_push<W, MT>(C, k) : filter_push<W, MT>(C, k);
         if (!ok) continue;
         if (k + 1 == t) {
@@ -1707,9 +1746,10 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
             if (C.lane == 0) {
                 S.iter[k] = 0;
                 S.iter_end[k] = S.lev[k].cnt[S.lev[k].branch];
+                if constexpr (kCons) S.cbase[k] = -1;
             }
             __syncwarp();
-            if constexpr (MT >= 5) {
+            if constexpr (kCons) {
                 if (k >= 3 && P.prune == 2) cons_prepare<W, MT>(C, k);
             }
         }
@@ -2023,9 +2063,11 @@ template <int W, int MT>
 cudaError_t set_smem_t(size_t bytes) {
     cudaError_t e = cudaFuncSetAttribute(search_kernel<W, MT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
-    if (e == cudaSuccess && has_deep<W, MT>())
-        e = cudaFuncSetAttribute(search_kernel<W, MT, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes));
+    if constexpr (has_deep<W, MT>()) {
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(search_kernel<W, MT, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(bytes));
+    }
     return e;
 }
 
@@ -2058,11 +2100,13 @@ cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, s
     const int mt = P.t < 2 ? 2 : P.t;
 #define PMS8G_CASE(WW, M)                                                 \
     if (W == WW && mt == M) {                                             \
-        if (has_deep<WW, M>() && warps <= 12)                             \
-            search_kernel<WW, M, (has_deep<WW, M>() ? 12 : 16)>           \
-                <<<blocks, warps * 32, smem, s>>>(P);                     \
-        else                                                              \
-            search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P); \
+        if constexpr (has_deep<WW, M>()) {                                \
+            if (warps <= 12) {                                            \
+                search_kernel<WW, M, 12><<<blocks, warps * 32, smem, s>>>(P); \
+                return cudaGetLastError();                                \
+            }                                                             \
+        }                                                                 \
+        search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P);     \
         return cudaGetLastError();                                        \
     }
     PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)

@@ -180,7 +180,7 @@ def test_cli_solve_matches_reference_stdout(tmp_path):
     r = subprocess.run([exe, "solve", str(f)], capture_output=True, text=True)
     assert r.returncode == 0
     assert r.stdout.split() == golden("planted_13_4.json")[0]["motifs"]
-    assert r.stderr.startswith("motifs=9 threshold=")
+    assert r.stderr.startswith("motifs=9 threshold=2 ")
     r = subprocess.run([exe, "solve", str(f), "--format", "json"], capture_output=True, text=True)
     assert json.loads(r.stdout)["motifs"] == golden("planted_13_4.json")[0]["motifs"]
     # no motif -> exit 1 (tools/pms8.cpp:183)
