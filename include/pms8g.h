@@ -76,6 +76,10 @@ typedef struct pms8g_options {
                               reference's shared atomic job counter src/parallel.cpp:54-60 across GPUs):
                               every rank searches all S1 l-mers, claiming (S1 l-mer, depth-1 branch) tasks
                               from one counter; exclusive with shard_count > 1 */
+    uint32_t jitter_max_us; /* test hook (ParallelOptions::jitter_max_us, include/pms8/parallel.hpp:24-27):
+                               every claimed task first sleeps a seeded pseudo-random 0..jitter_max_us us,
+                               shaking the schedule; the motif set must not change */
+    uint64_t jitter_seed;
 } pms8g_options;
 
 /* Mirrors RunReport + SolveCounters (include/pms8/report.hpp:28-56). */

@@ -284,6 +284,8 @@ def _options(config: Optional[SolverConfig], par: Optional[ParallelOptions], win
     o.blocks_per_sm = int(par.blocks_per_sm)
     o.exact_tree = 1 if par.exact_tree else 0
     o.grid_blocks = int(par.grid_blocks)
+    o.jitter_max_us = int(par.jitter_max_us)
+    o.jitter_seed = int(par.jitter_seed)
     if par.queue is not None:
         o.queue = par.queue.ptr
     keep = None

@@ -36,6 +36,8 @@ class Options(ctypes.Structure):
         ("nbranches", ctypes.c_int),
         ("grid_blocks", ctypes.c_int),
         ("queue", ctypes.c_void_p),
+        ("jitter_max_us", ctypes.c_uint32),
+        ("jitter_seed", ctypes.c_uint64),
     ]
 
 

@@ -56,6 +56,9 @@ struct GpuOptions {
     // several GPUs of this process as the worker team (pms8g_solve_multi):
     // shared task counter over NVLink, NCCL allgather of the motif sets
     std::vector<int> devices;
+    // ParallelOptions' schedule-shaking test hook (include/pms8/parallel.hpp:24-27)
+    uint32_t jitter_max_us = 0;
+    uint64_t jitter_seed = 0;
 };
 
 struct SolveCounters {

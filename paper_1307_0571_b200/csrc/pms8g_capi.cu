@@ -535,6 +535,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     const int na = static_cast<int>(c->anchors.size());
     c->level_cap = (c->K + 31) / 32 * 32;  // keeps the per-warp node overflow 16-byte aligned
     c->node_cap = 64 * (l + 4);
+    if (const char* e = std::getenv("PMS8G_NODE_CAP")) c->node_cap = std::max(0, std::atoi(e));  // failure tests
     const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
     const size_t node_words = static_cast<size_t>(c->node_cap) * node_bytes(c->W) / 4;
     c->scratch_words = (lvl_words + node_words + 64 + 31) / 32 * 32;  // + consensus masks (cons_slot)
@@ -554,7 +555,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     AL(c->d_key_count, sizeof(unsigned long long));
     AL(c->d_unique_count, sizeof(long long));
     AL(c->d_counters, sizeof(unsigned long long) * C_NCTR);
-    AL(c->d_err, sizeof(int));
+    AL(c->d_err, 2 * sizeof(int));  // flags, failing S1 offset + 1
     AL(c->d_task_ai, sizeof(int32_t) * std::max<size_t>(1, c->task_ai.size()));
     AL(c->d_task_u, sizeof(uint32_t) * std::max<size_t>(1, c->task_u.size()));
     if (c->task_u.empty() && t >= 2 && !std::getenv("PMS8G_NO_TASK_ORDER")) {
@@ -1095,7 +1096,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         CU(cudaMemsetAsync(c->d_key_count, 0, sizeof(unsigned long long), s));
         CU(cudaMemsetAsync(c->d_qs, 0, sizeof(QueueState), s));
         CU(cudaMemsetAsync(c->d_qstate, 0, sizeof(unsigned int) * c->qcap, s));
-        CU(cudaMemsetAsync(c->d_err, 0, sizeof(int), s));
+        CU(cudaMemsetAsync(c->d_err, 0, 2 * sizeof(int), s));
         CU(cudaMemsetAsync(c->d_fail, 0, sizeof(int), s));
         CU(launch_encode(c->W, c->d_codes, c->n, c->m, c->l, c->w, c->d_table, c->d_err, s));
         CU(cudaEventRecord(c->ev[0], s));
@@ -1159,6 +1160,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.key_cap = c->key_cap;
         P.counters = c->d_counters;
         P.error_flag = c->d_err;
+        P.jitter_ns = 1000ull * c->opt.jitter_max_us;
+        P.jitter_seed = c->opt.jitter_seed;
         P.gqueue = nullptr;
         P.gepoch = 0;
         if (c->opt.queue && attempt == 0) {
@@ -1187,7 +1190,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
                            s));
         CU(cudaMemcpyAsync(c->h_counters + C_NCTR, c->d_key_count, sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(c->h_err, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         CU(cudaGetLastError());
         if (d_tl) {
@@ -1201,13 +1204,17 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             }
         }
         if (c->h_err[0] & 1) return fail(err, errlen, PMS8G_ERR_INVALID, "symbol code outside the 2-bit alphabet");
+        // worker failures name the subproblem like run_parallel (src/parallel.cpp:66-86)
+        char where[64] = "search";
+        if (c->h_err[1] > 0) std::snprintf(where, sizeof where, "subproblem at offset %d", c->h_err[1] - 1);
         if (c->h_err[0] & 2)
-            return fail(err, errlen, PMS8G_ERR_RUNTIME, "enumeration stack overflow (l=%d, capacity %d nodes)", c->l,
-                        c->node_cap);
+            return fail(err, errlen, PMS8G_ERR_RUNTIME, "%s failed: enumeration stack overflow (l=%d, capacity %d nodes)",
+                        where, c->l, c->node_cap);
         if (c->h_err[0] & 8)
-            return fail(err, errlen, PMS8G_ERR_RUNTIME, "search work queue watchdog fired (no progress)");
+            return fail(err, errlen, PMS8G_ERR_RUNTIME, "search failed: work queue watchdog fired (no progress)");
         if (c->h_err[0] & 4)
-            return fail(err, errlen, PMS8G_ERR_LOGIC, "replay of a donated task diverged from its donor");
+            return fail(err, errlen, PMS8G_ERR_LOGIC, "%s failed: replay of a donated task diverged from its donor",
+                        where);
         const long long raw = static_cast<long long>(c->h_counters[C_NCTR]);
         if (c->opt.max_motifs >= 0 && raw > c->opt.max_motifs)
             return fail(err, errlen, PMS8G_ERR_RUNTIME, "motif cap of %lld exceeded",
@@ -1235,11 +1242,11 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
                 CU(cudaStreamSynchronize(s));
                 uniq = static_cast<long long>(c->h_counters[C_NCTR + 1]);
                 CU(launch_reverify(c->W, c->d_table, c->n, c->w, c->l, c->d, c->d_keys_unique, uniq, c->d_fail, s));
-                CU(cudaMemcpyAsync(c->h_err + 1, c->d_fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CU(cudaMemcpyAsync(c->h_err + 2, c->d_fail, sizeof(int), cudaMemcpyDeviceToHost, s));
             }
             CU(cudaStreamSynchronize(s));
             uniq = static_cast<long long>(c->h_counters[C_NCTR + 1]);
-            if (c->opt.reverify && c->h_err[1])
+            if (c->opt.reverify && c->h_err[2])
                 return fail(err, errlen, PMS8G_ERR_LOGIC, "re-verification failed for a reported motif");
         }
         c->unique_count = uniq;

@@ -59,6 +59,8 @@ MotifSet run_parallel(const Problem& problem, const SolverConfig& config, const 
     o.device = options.device;
     o.shard_rank = options.shard_rank;
     o.shard_count = options.shard_count;
+    o.jitter_max_us = options.jitter_max_us;
+    o.jitter_seed = options.jitter_seed;
     if (!options.anchors.empty()) {
         o.anchors = options.anchors.data();
         o.nanchors = static_cast<int>(options.anchors.size());

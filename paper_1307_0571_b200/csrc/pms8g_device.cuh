@@ -69,7 +69,7 @@ struct QueueState {
     unsigned long long static_next;  // next static task
     unsigned long long head;         // next dynamic slot to consume
     unsigned long long alloc;        // dynamic slots reserved by producers
-    unsigned long long ready_unused;
+    unsigned long long heartbeat;    // bumped by busy warps while others wait (watchdog)
     unsigned int busy;               // warps holding a task
     unsigned int waiting;            // warps idle, waiting for work
     unsigned long long pad[4];
@@ -137,6 +137,9 @@ struct SearchParams {
     // shared by every rank over NVLink: value = epoch << 40 | next task
     unsigned long long* gqueue;
     unsigned long long gepoch;
+    // test hook: sleep a seeded pseudo-random 0..jitter_ns ns before each task
+    unsigned long long jitter_ns;
+    unsigned long long jitter_seed;
 };
 
 constexpr int GQ_SHIFT = 40;

@@ -78,6 +78,7 @@ struct WarpCtx {
     int anchor;          // anchor index of the current task
     int lane;
     int pushes_since_check;
+    unsigned int checks;  // starvation checks made (lane 0; heartbeat pacing)
     // shared-memory views derived from the extern __shared__ symbol, so every
     // access compiles to LDS/STS rather than generic LD/ST
     __device__ __forceinline__ const Lmer<W>* T() const { return reinterpret_cast<const Lmer<W>*>(dyn_smem); }
@@ -118,6 +119,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
     unsigned long long v;
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Record a failure and the S1 offset of the subproblem it happened in (the
+// first failure wins), so the host can name it like run_parallel does
+// (src/parallel.cpp:66-86). error_flag[1] = S1 offset + 1 (0: none).
+template <int W, int MT>
+__device__ __forceinline__ void raise_error(const WarpCtx<W, MT>& C, int bit) {
+    atomicOr(C.P->error_flag, bit);
+    atomicCAS(C.P->error_flag + 1, 0, C.P->anchor_off[C.anchor] + 1);
 }
 
 // ---------------------------------------------------------------- static tasks
@@ -451,6 +461,8 @@ __device__ bool starving(WarpCtx<W, MT>& C) {
     if (C.lane == 0) {
         const unsigned int waiting = ld_volatile(&P.qs->waiting);
         if (waiting > 0) {
+            // heartbeat for the waiters' watchdog: busy warps are making progress
+            if ((++C.checks & 7) == 0) atomicAdd(&P.qs->heartbeat, 1ull);
             const unsigned long long alloc = ld_volatile(&P.qs->alloc), head = ld_volatile(&P.qs->head);
             const unsigned long long queued = alloc > head ? alloc - head : 0;
             want = queued < waiting;
@@ -466,6 +478,7 @@ __device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k
     if (!C.P->donate) return;
     if (++C.pushes_since_check < C.P->don_pushes) return;
     C.pushes_since_check = 0;
+    C.checks = 0;
     if (!starving<W, MT>(C)) return;
     WarpFixed& S = *C.S();
     for (int kk = kmin; kk <= k; ++kk) {
@@ -1306,7 +1319,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
             bool overflow = false;
             while (nn > NS - 48) {
                 if (nov + SPILL > P.node_cap) {
-                    if (lane == 0) atomicOr(P.error_flag, 2);
+                    if (lane == 0) raise_error<1, MT>(C, 2);
                     overflow = true;
                     break;
                 }
@@ -1636,7 +1649,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
         bool overflow = false;
         while (nn > NS - 48) {  // spill bottom chunks: a round may add 48 nodes net
             if (nov + SPILL > P.node_cap) {
-                if (lane == 0) atomicOr(P.error_flag, 2);
+                if (lane == 0) raise_error<W, MT>(C, 2);
                 overflow = true;
                 break;
             }
@@ -1815,7 +1828,8 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     QueueState* qs = P.qs;
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
     bool waiting = false;
-    long long wait_t0 = 0;
+    long long wait_t0 = 0, beat_t0 = 0;
+    unsigned long long beat = 0;
     unsigned int backoff = 128;
 
     for (;;) {
@@ -1849,14 +1863,22 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                 if (!waiting) {
                     atomicAdd(&qs->waiting, 1u);
                     waiting = true;
-                    wait_t0 = clock64();
+                    wait_t0 = beat_t0 = clock64();
+                    beat = ld_volatile(&qs->heartbeat);
                     backoff = 128;
+                }
+                const unsigned long long b = ld_volatile(&qs->heartbeat);
+                if (b != beat) {  // somebody is still working: not stuck
+                    beat = b;
+                    beat_t0 = clock64();
                 }
                 if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
                     !statics_left(P, nstatic)) {
                     kind = 2;
-                } else if (clock64() - wait_t0 > (1ll << 35)) {
-                    atomicOr(P.error_flag, 8);  // watchdog: ~17 s without work
+                } else if (clock64() - beat_t0 > (1ll << 37)) {
+                    // watchdog: ~70 s with busy warps but no heartbeat (they
+                    // beat every few starvation checks): a lost task
+                    atomicOr(P.error_flag, 8);
                     kind = 2;
                 } else {
                     // idle warps back off so their polling does not steal
@@ -1880,6 +1902,19 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             break;
         }
         if (kind < 0) continue;
+        if (P.jitter_ns && lane == 0) {
+            // schedule-shaking test hook (run_parallel's jitter, src/parallel.cpp:57-65)
+            unsigned long long z = P.jitter_seed + 0x9E3779B97F4A7C15ull * (idx + 1 + (static_cast<unsigned long long>(kind) << 40) +
+                                                                        (static_cast<unsigned long long>(gw) << 44));
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            unsigned long long ns = (z ^ (z >> 31)) % (P.jitter_ns + 1);
+            while (ns > 0) {
+                const unsigned int step = static_cast<unsigned int>(ns < 1000000ull ? ns : 1000000ull);
+                __nanosleep(step);
+                ns -= step;
+            }
+        }
         const long long task_t0 = clock64();
         if ((P.timeline || P.log_cycles) && lane == 0) {
             // diagnostics only; kept in shared memory, not in registers
@@ -1968,7 +2003,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                 S.diag[2] = S.ctr[W_NODES] - static_cast<unsigned long long>(tdiag[2]);
             }
             if (!ok) {
-                if (lane == 0) atomicOr(P.error_flag, 4);
+                if (lane == 0) raise_error<W, MT>(C, 4);
             } else if (S.task.kind == 0) {
                 dfs<W, MT>(C, tk, S.task.a0, S.task.a1);
             } else {

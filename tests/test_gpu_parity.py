@@ -306,3 +306,22 @@ def test_shared_queue_ranks_claim_every_task_once(tmp_path, world, l, d, seed):
         assert run["motifs"] == want
         assert run["statics"] == res["nstatic"]
     assert res["api"] == want
+
+
+def test_jitter_hook_keeps_the_motif_set():
+    # ParallelOptions' schedule-shaking hook (include/pms8/parallel.hpp:24-27):
+    # every task sleeps a seeded random time first; the output must not change
+    g = golden("planted_13_4.json")[0]
+    inst = planted(13, 4, 1)
+    for seed in (1, 2):
+        got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(jitter_max_us=40, jitter_seed=seed))
+        assert got == g["motifs"]
+
+
+def test_worker_failure_names_the_subproblem(monkeypatch):
+    # run_parallel aborts naming the failing offset (src/parallel.cpp:66-86);
+    # a zero-capacity node overflow stack makes the first deep enumeration fail
+    monkeypatch.setenv("PMS8G_NODE_CAP", "0")
+    inst = planted(17, 6, 1)
+    with pytest.raises(P.SolverRuntimeError, match=r"^subproblem at offset \d+ failed: enumeration stack overflow"):
+        P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=list(range(0, 584, 8))))
