@@ -529,6 +529,9 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     c->warps = warps;
     c->smem = search_smem(c->W, c->K, warps, c->plan);
     c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
+    // clusters of search_cluster(W) CTAs share the l-mer table: whole clusters only
+    const int cs = search_cluster(c->W);
+    c->blocks = std::max(cs, c->blocks / cs * cs);
     if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
         return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
 
@@ -1150,6 +1153,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         if (const char* e = std::getenv("PMS8G_DON_ROUNDS")) P.don_rounds_mask = std::max(1, std::atoi(e)) - 1;
         P.lazy = (c->opt.exact_tree || std::getenv("PMS8G_EAGER")) ? 0 : 1;
         P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
+        // the consensus row rule changes the tree (not the motif set): off for exact_tree
+        P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
         P.plan = c->plan;
         P.scratch = c->d_scratch;
         P.scratch_words = c->scratch_words;

@@ -57,6 +57,7 @@ enum Ctr {
     C_LOG0,                          // 32 records x 8 words: kind, anchor, idx, cycles, tuples, leaves, nodes, vcmp
     C_TLN = C_LOG0 + 256,            // diagnostics: timeline records written
     C_STATIC,                        // static tasks claimed by this device
+    C_CONS_REJ,                      // slots rejected by the stack consensus row rule
     C_NCTR
 };
 
@@ -140,6 +141,7 @@ struct SearchParams {
     // test hook: sleep a seeded pseudo-random 0..jitter_ns ns before each task
     unsigned long long jitter_ns;
     unsigned long long jitter_seed;
+    int cons_rows;  // 1: push filters apply the stack consensus bound to every remaining row
 };
 
 constexpr int GQ_SHIFT = 40;

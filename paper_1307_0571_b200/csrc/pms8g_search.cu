@@ -43,6 +43,18 @@ struct NodeSmem {
     static constexpr int N = W == 1 ? 128 : 64;  // power of two
 };
 
+enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
+            W_DONATED, W_REPLAYS, W_CLKF, W_CLKP, W_CONSREJ, W_N };
+
+// Wait state of a warp's claim loop (lane 0 only; shared memory, so the
+// persistent loop keeps no registers for it).
+struct WaitState {
+    int waiting;
+    unsigned int backoff;
+    long long wait_t0, beat_t0;
+    unsigned long long beat;
+};
+
 struct WarpFixed {
     LevelMeta lev[MAXT + 1];
     int iter[MAXT + 1];
@@ -53,20 +65,20 @@ struct WarpFixed {
     uint8_t perm[64];            // enumeration depth -> l-mer position of the current tuple
     unsigned long long diag[5];  // diagnostics: counters at task start + start time (ns)
     TaskHeader task;
-    unsigned long long ctr[16];  // per-warp counters (lane 0 updates)
+    unsigned long long ctr[W_N];  // per-warp counters (lane 0 updates)
     uint32_t lazy_mask;          // rows of the lazy level already filtered
     int lazy_level;              // level whose rows are filtered on demand (0: none)
-    // consensus prefilter of the branching row (levels whose push adds a 4th+
-    // member): bit i = entry cbase[k] + i passed cons_check, for 32 entries
-    // evaluated lane-parallel at once; cbase < 0: nothing cached
-    uint32_t cmask[MAXT + 1];
-    int32_t cbase[MAXT + 1];
+    WaitState wait;              // claim loop state (lane 0)
 };
 
-enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
-            W_DONATED, W_REPLAYS, W_CLKF, W_CLKP, W_N };
 
 constexpr int MAXCH = 5;  // candidate chunks of 32 held in registers by verify
+
+// Two-word l-mers (16 B each) would take 176 KB of a 227 KB CTA for n=20,
+// m=600, leaving room for 7 warps; split over a 2-CTA cluster each SM holds
+// 88 KB and runs 16 warps.
+template <int W>
+constexpr bool kClusterTable = W == 2;
 
 template <int W, int MT>
 struct WarpCtx {
@@ -79,9 +91,35 @@ struct WarpCtx {
     int lane;
     int pushes_since_check;
     unsigned int checks;  // starvation checks made (lane 0; heartbeat pacing)
+    // two-word l-mers: the table is split over the CTA pair of a cluster
+    // (ids < thalf in rank 0's shared memory, the rest in rank 1's), read
+    // through distributed shared memory; tb[r] = shared::cluster address of
+    // rank r's half
+    uint32_t tb[2];
+    uint32_t thalf;
     // shared-memory views derived from the extern __shared__ symbol, so every
     // access compiles to LDS/STS rather than generic LD/ST
     __device__ __forceinline__ const Lmer<W>* T() const { return reinterpret_cast<const Lmer<W>*>(dyn_smem); }
+    // l-mer `id` of the table (one-word: local LDS.64; two-word: one
+    // LD.shared::cluster.v4 from whichever CTA of the pair holds it)
+    __device__ __forceinline__ Lmer<W> lmer(uint32_t id) const {
+        if constexpr (kClusterTable<W>) {
+            const uint32_t r = id >= thalf ? 1u : 0u;
+            const uint32_t addr = tb[r] + (id - r * thalf) * static_cast<uint32_t>(sizeof(Lmer<W>));
+            uint32_t a, b, c, e;
+            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
+                         : "r"(addr));
+            Lmer<W> x;
+            x.h[0] = a;
+            x.h[W - 1] = b;
+            x.o[0] = c;
+            x.o[W - 1] = e;
+            return x;
+        } else {
+            return T()[id];
+        }
+    }
     __device__ __forceinline__ WarpFixed* S() const { return reinterpret_cast<WarpFixed*>(dyn_smem + off_S); }
     __device__ __forceinline__ uint8_t* thr() const { return dyn_smem + off_thr; }
     __device__ __forceinline__ Lmer<W>* cand() const { return reinterpret_cast<Lmer<W>*>(dyn_smem + off_cand); }
@@ -130,6 +168,21 @@ __device__ __forceinline__ void raise_error(const WarpCtx<W, MT>& C, int bit) {
     atomicCAS(C.P->error_flag + 1, 0, C.P->anchor_off[C.anchor] + 1);
 }
 
+// Schedule-shaking test hook (run_parallel's jitter, src/parallel.cpp:57-65):
+// sleep a seeded pseudo-random 0..jitter_ns ns (out of line: it must not cost
+// the persistent loop registers).
+__device__ __noinline__ void jitter_sleep(const SearchParams& P, unsigned long long key) {
+    unsigned long long z = P.jitter_seed + 0x9E3779B97F4A7C15ull * key;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    unsigned long long ns = (z ^ (z >> 31)) % (P.jitter_ns + 1);
+    while (ns > 0) {
+        const unsigned int step = static_cast<unsigned int>(ns < 1000000ull ? ns : 1000000ull);
+        __nanosleep(step);
+        ns -= step;
+    }
+}
+
 // ---------------------------------------------------------------- static tasks
 // Static tasks come from the device-local counter, or (multi-GPU) from the
 // shared queue counter every rank claims from over NVLink. The shared counter
@@ -170,6 +223,190 @@ __device__ __forceinline__ bool claim_static(const SearchParams& P, unsigned lon
     }
 }
 
+// Stack consensus bound as a row filter. m l-mers have a common d-neighbour
+// only if their consensus cost (sum over columns of m minus the most frequent
+// symbol's count) is at most m*d; the witness v of a motif in any remaining
+// row forms such a set with the stack, so a push may drop every row entry v
+// for which stack + v fails the bound — a sound rule like Theorem 1, applied
+// by the push filters next to the pair and triple rules once stack + v has 4+
+// members (for 3 members Theorem 1 is exact). Incremental form: for the k
+// members stack[0..k-1], G[c] = positions where symbol c is a plurality
+// symbol (count == the column maximum M) and need = (k+1)(l-d) - sum M,
+// computed once per push (cons_prepare, slot k); then v passes iff
+// popc(sum over c of G[c] & [v == c]) >= need (adding v raises a column's
+// maximum exactly where v holds a plurality symbol). Kept in the warp's
+// global scratch, 4W+1 words per slot.
+template <int W, int MT>
+__device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
+    const SearchParams& P = *C.P;
+    return C.lvl_glob + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap +
+           static_cast<size_t>(P.node_cap) * (sizeof(Node<W>) / 4) + 9 * k;
+}
+
+template <int W, int MT>
+__device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k) {
+    const SearchParams& P = *C.P;
+    const WarpFixed& S = *C.S();
+    const int l = P.l;
+    uint32_t* slot = cons_slot<W, MT>(C, k);
+    int sum_m = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int nb = min(32, l - 32 * w);
+        const uint32_t lm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
+        uint32_t ge[4][MT + 1];  // ge[c][j]: at least j members hold c (j <= k)
+        uint32_t mg[MT + 1];
+#pragma unroll
+        for (int j = 0; j <= MT; ++j) mg[j] = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            ge[c][0] = lm;
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) ge[c][j] = 0u;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                if (i < k) {
+                    const Lmer<W> x = C.lmer(S.stack_id[i] & ID_MASK);
+                    const uint32_t e = ((c & 2) ? x.h[w] : ~x.h[w]) & ((c & 1) ? x.o[w] : ~x.o[w]) & lm;
+#pragma unroll
+                    for (int j = MT; j >= 1; --j) ge[c][j] |= ge[c][j - 1] & e;
+                }
+            }
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) mg[j] |= ge[c][j];
+        }
+#pragma unroll
+        for (int j = 1; j <= MT; ++j) sum_m += __popc(mg[j]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t g = 0u;
+#pragma unroll
+            for (int j = 1; j <= MT; ++j) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
+            if (C.lane == c * W + w) slot[c * W + w] = g;
+        }
+    }
+    if (C.lane == 4 * W) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - sum_m);
+    __syncwarp();
+}
+
+template <int W, int MT>
+__device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint32_t u) {
+    const uint32_t* slot = cons_slot<W, MT>(C, k);
+    const Lmer<W> x = C.lmer(u & ID_MASK);
+    int matches = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t h = x.h[w], o = x.o[w];
+        const uint32_t hit = (slot[0 * W + w] & ~h & ~o) | (slot[1 * W + w] & ~h & o) |
+                             (slot[2 * W + w] & h & ~o) | (slot[3 * W + w] & h & o);
+        matches += __popc(hit);
+    }
+    return matches >= static_cast<int>(slot[4 * W]);
+}
+
+// The slot's masks hoisted into registers for a filter pass.
+template <int W>
+struct ConsMasks {
+    uint32_t g[4][W];
+    int need;
+};
+
+template <int W, int MT>
+__device__ __forceinline__ ConsMasks<W> load_cons(const WarpCtx<W, MT>& C, int k) {
+    const uint32_t* slot = cons_slot<W, MT>(C, k);
+    ConsMasks<W> cm;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int w = 0; w < W; ++w) cm.g[c][w] = slot[c * W + w];
+    cm.need = static_cast<int>(slot[4 * W]);
+    return cm;
+}
+
+template <int W>
+__device__ __forceinline__ bool cons_pass(const ConsMasks<W>& cm, const Lmer<W>& x) {
+    int matches = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t h = x.h[w], o = x.o[w];
+        matches += __popc((cm.g[0][w] & ~(h | o)) | (cm.g[1][w] & o & ~h) | (cm.g[2][w] & h & ~o) |
+                          (cm.g[3][w] & h & o));
+    }
+    return matches >= cm.need;
+}
+
+// Pushes whose filter applies the consensus row rule: stack + v has 4+
+// members (k >= 2), full pruning, t >= 4 builds.
+template <int MT>
+__device__ __forceinline__ bool cons_rows_at(const SearchParams& P, int k) {
+    return MT >= 4 && P.cons_rows && k >= 2;
+}
+
+// One claim attempt by lane 0: 0 static task, 1 dynamic task (idx set),
+// 2 terminate, -1 nothing yet (backed off). Protocol in DESIGN.md §4.
+__device__ __noinline__ int claim_task(const SearchParams& P, unsigned long long nstatic, WaitState& ws,
+                                       unsigned long long& idx) {
+    QueueState* qs = P.qs;
+    const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
+    int kind = -1;
+    const bool have_static = statics_left(P, nstatic);
+    const unsigned long long h0 = ld_volatile(&qs->head);
+    const bool have_dyn = ld_volatile(&P.qstate[h0 % qcap]) == 2u * static_cast<unsigned int>(h0 / qcap) + 1u;
+    if (have_static || have_dyn) {
+        // announce before claiming so that no waiter can observe
+        // busy == 0 while a claimed task is still unannounced
+        atomicAdd(&qs->busy, 1u);
+        if (have_static && claim_static(P, nstatic, idx)) {
+            kind = 0;
+            atomicAdd(P.counters + C_STATIC, 1ull);
+        }
+        if (kind < 0) {
+            const unsigned long long h = ld_volatile(&qs->head);
+            if (ld_volatile(&P.qstate[h % qcap]) == 2u * static_cast<unsigned int>(h / qcap) + 1u &&
+                atomicCAS(&qs->head, h, h + 1) == h) {
+                kind = 1;
+                idx = h;
+                __threadfence();
+            }
+        }
+        if (kind < 0) atomicSub(&qs->busy, 1u);
+    }
+    if (kind < 0) {
+        if (!ws.waiting) {
+            atomicAdd(&qs->waiting, 1u);
+            ws.waiting = 1;
+            ws.wait_t0 = ws.beat_t0 = clock64();
+            ws.beat = ld_volatile(&qs->heartbeat);
+            ws.backoff = 128;
+        }
+        const unsigned long long b = ld_volatile(&qs->heartbeat);
+        if (b != ws.beat) {  // somebody is still working: not stuck
+            ws.beat = b;
+            ws.beat_t0 = clock64();
+        }
+        if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
+            !statics_left(P, nstatic)) {
+            kind = 2;
+        } else if (clock64() - ws.beat_t0 > (1ll << 37)) {
+            // watchdog: ~70 s with busy warps but no heartbeat (they beat
+            // every few starvation checks while others wait): a lost task
+            atomicOr(P.error_flag, 8);
+            kind = 2;
+        } else {
+            // idle warps back off so their polling does not steal issue
+            // slots and L2 bandwidth from the busy ones
+            __nanosleep(ws.backoff);
+            ws.backoff = min(ws.backoff * 2, 8192u);
+        }
+    }
+    if (kind >= 0 && ws.waiting) {
+        atomicSub(&qs->waiting, 1u);
+        ws.waiting = 0;
+        atomicAdd(P.counters + C_IDLE, static_cast<unsigned long long>(clock64() - ws.wait_t0));
+    }
+    return kind;
+}
+
 // ---------------------------------------------------------------- push filter
 // Push of u = stack[k] onto a stack of k members: filter level k (minus its
 // branching row) into level k+1. Returns viable (no remaining row emptied).
@@ -185,17 +422,23 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const int d = P.d, six_d = 6 * d, two_d = 2 * d;
     const long long f0 = clock64();
 
-    const Lmer<W> U = C.T()[S.stack_id[k] & ID_MASK];
+    const Lmer<W> U = C.lmer(S.stack_id[k] & ID_MASK);
     Lmer<W> Sm[MT];
     Mask<W> Miu[MT];
     int hs[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         if (i < k) {
-            Sm[i] = C.T()[S.stack_id[i] & ID_MASK];
+            Sm[i] = C.lmer(S.stack_id[i] & ID_MASK);
             Miu[i] = mism<W>(Sm[i], U);
             hs[i] = popcm<W>(Miu[i]);
         }
+    }
+    const bool cons = cons_rows_at<MT>(P, k);
+    ConsMasks<W> cm;
+    if (cons) {
+        cons_prepare<W, MT>(C, k + 1);
+        cm = load_cons<W, MT>(C, k + 1);
     }
     const int jb = Ls.branch;
     const int bstart = Ls.start[jb], bcnt = Ls.cnt[jb];
@@ -205,7 +448,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     if (lane == 0) S.lazy_level = 0;
     __syncwarp();
     int out = 0;
-    unsigned pair_rej = 0, tri_rej = 0;
+    unsigned pair_rej = 0, tri_rej = 0, cons_rej = 0;
     // the next block's entries are loaded one iteration ahead (the level
     // entries stream from L2; this hides one load latency per block)
     auto load_entry = [&](int f) -> uint32_t {
@@ -219,11 +462,15 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         e_next = load_entry(f + 32);
         bool keep = false;
         if (valid) {
-            const Lmer<W> V = C.T()[e & ID_MASK];
+            const Lmer<W> V = C.lmer(e & ID_MASK);
             const Mask<W> mu = mism<W>(V, U);
             const int hvu = popcm<W>(mu);
             keep = hvu <= two_d;
             pair_rej += !keep;
+            if (cons && keep) {
+                keep = cons_pass<W>(cm, V);
+                cons_rej += !keep;
+            }
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 if (i < k && keep) {
@@ -255,14 +502,16 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     C.add(W_PUSH, 1);
     C.add(W_SLOTS, static_cast<unsigned long long>(n_iter));
     {
-        unsigned pr = pair_rej, tr = tri_rej;
+        unsigned pr = pair_rej, tr = tri_rej, cr = cons_rej;
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             pr += __shfl_xor_sync(0xffffffffu, pr, sh);
             tr += __shfl_xor_sync(0xffffffffu, tr, sh);
+            cr += __shfl_xor_sync(0xffffffffu, cr, sh);
         }
         C.add(W_PAIRREJ, pr);
         C.add(W_TRIREJ, tr);
+        C.add(W_CONSREJ, cr);
     }
     bool ok = true;
     {
@@ -322,14 +571,18 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     uint32_t* dst = level_entries<W, MT>(C, k + 1) + Ls.start[j];
     const int cnt = Ls.cnt[j];
     const int d = P.d, six_d = 6 * d, two_d = 2 * d;
-    const Lmer<W> U = C.T()[S.stack_id[k] & ID_MASK];
+    // consensus row rule: slot k + 1 was prepared by the lazy push
+    const bool cons = cons_rows_at<MT>(P, k);
+    ConsMasks<W> cm;
+    if (cons) cm = load_cons<W, MT>(C, k + 1);
+    const Lmer<W> U = C.lmer(S.stack_id[k] & ID_MASK);
     Lmer<W> Sm[MT];
     Mask<W> Miu[MT];
     int hs[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         if (i < k) {
-            Sm[i] = C.T()[S.stack_id[i] & ID_MASK];
+            Sm[i] = C.lmer(S.stack_id[i] & ID_MASK);
             Miu[i] = mism<W>(Sm[i], U);
             hs[i] = popcm<W>(Miu[i]);
         }
@@ -342,10 +595,11 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
         const uint32_t e = e_next;
         e_next = f + 32 < cnt ? src[f + 32] : 0u;
         if (f < cnt) {
-            const Lmer<W> V = C.T()[e & ID_MASK];
+            const Lmer<W> V = C.lmer(e & ID_MASK);
             const Mask<W> mu = mism<W>(V, U);
             const int hvu = popcm<W>(mu);
             keep = hvu <= two_d;
+            if (cons && keep) keep = cons_pass<W>(cm, V);
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 if (i < k && keep) {
@@ -380,6 +634,7 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
     const int jb = Ls.branch;
     const int nr2 = Ls.nrows - 1;
     const long long f0 = clock64();
+    if (cons_rows_at<MT>(*C.P, k)) cons_prepare<W, MT>(C, k + 1);  // for filter_one_row
     int c = 0x7FFF;
     if (lane < nr2) {
         const int j = lane < jb ? lane : lane + 1;
@@ -509,9 +764,9 @@ __device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k
 // loaded once (32 per coalesced load) and broadcast by shuffle, and each
 // compare instruction covers 32 x NCH candidate/entry pairs. Survivors are
 // compacted to the front of the buffer; returns their number.
-template <int W, int NCH>
-__device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const uint32_t* entries, int st, int cnt,
-                                         int n, int d, int lane, int& scanned) {
+template <int W, int MT, int NCH>
+__device__ __forceinline__ int verify_row(const WarpCtx<W, MT>& C, Lmer<W>* cand, const uint32_t* entries, int st,
+                                         int cnt, int n, int d, int lane, int& scanned) {
     Lmer<W> cd[NCH];
     bool alive[NCH];
     int hm[NCH];  // smallest distance to the entries scanned so far (dead lanes: 0)
@@ -528,7 +783,7 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
         // blocks of U entries can be compared without bound checks (a
         // duplicate cannot change "some entry is within d")
         const int lim = min(32, cnt - eb);
-        const Lmer<W> mine = T[entries[st + eb + (lane < lim ? lane : 0)] & ID_MASK];
+        const Lmer<W> mine = C.lmer(entries[st + eb + (lane < lim ? lane : 0)] & ID_MASK);
         for (int x0 = 0; x0 < lim; x0 += U) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -563,14 +818,14 @@ __device__ __forceinline__ int verify_row(const Lmer<W>* T, Lmer<W>* cand, const
 // Few candidates (n <= 12): lanes hold row entries instead, and each
 // candidate is checked against 32 entries per ballot, stopping at its first
 // witness.
-template <int W>
-__device__ __forceinline__ int verify_row_small(const Lmer<W>* T, Lmer<W>* cand, const uint32_t* entries, int st,
-                                               int cnt, int n, int d, int lane, int& scanned) {
+template <int W, int MT>
+__device__ __forceinline__ int verify_row_small(const WarpCtx<W, MT>& C, Lmer<W>* cand, const uint32_t* entries,
+                                               int st, int cnt, int n, int d, int lane, int& scanned) {
     unsigned pass = 0u;  // bit i: candidate i has a witness in this row
     for (int eb = 0; eb < cnt; eb += 32) {
         const bool have = eb + lane < cnt;
         Lmer<W> mine;
-        if (have) mine = T[entries[st + eb + lane] & ID_MASK];
+        if (have) mine = C.lmer(entries[st + eb + lane] & ID_MASK);
         for (int i = 0; i < n; ++i) {
             if ((pass >> i) & 1u) continue;
             const Lmer<W> c = cand[i];
@@ -622,11 +877,11 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
         const int st = L.start[j], cnt = L.cnt[j];
         int scanned = 0, out = 0;
         if (n <= 12) {
-            out = verify_row_small<W>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned);
+            out = verify_row_small<W, MT>(C, C.cand(), entries, st, cnt, n, d, lane, scanned);
         } else switch ((n + 31) >> 5) {
-            case 1: out = verify_row<W, 1>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-            case 2: out = verify_row<W, 2>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-            default: out = verify_row<W, 5>(C.T(), C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            case 1: out = verify_row<W, MT, 1>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            case 2: out = verify_row<W, MT, 2>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+            default: out = verify_row<W, MT, 5>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
         }
         vcmp += static_cast<unsigned long long>(n) * scanned;
         n = out;
@@ -1411,119 +1666,6 @@ __device__ __forceinline__ bool root_consensus_ok(const WarpCtx<W, MT>& C, int t
     return cost <= t * C.P->d;
 }
 
-// Incremental form of the stack consensus bound, used before every push of a
-// 4th+ member: for the k members below level k, G[c] = positions where symbol
-// c is a plurality symbol (count == the column maximum M) and
-// need = (k+1)(l-d) - sum M, computed once per level state; then u passes iff
-// popc(sum over c of G[c] & [u == c]) >= need (adding u raises a column's
-// maximum exactly where u holds a plurality symbol). Kept in the warp's
-// global scratch (L1-resident), 4W+1 words per level.
-template <int W, int MT>
-__device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
-    const SearchParams& P = *C.P;
-    return C.lvl_glob + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap +
-           static_cast<size_t>(P.node_cap) * (sizeof(Node<W>) / 4) + 9 * k;
-}
-
-template <int W, int MT>
-__device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k) {
-    const SearchParams& P = *C.P;
-    const WarpFixed& S = *C.S();
-    const int l = P.l;
-    uint32_t* slot = cons_slot<W, MT>(C, k);
-    int sum_m = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const int nb = min(32, l - 32 * w);
-        const uint32_t lm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
-        uint32_t ge[4][MT + 1];  // ge[c][j]: at least j members hold c (j <= k)
-        uint32_t mg[MT + 1];
-#pragma unroll
-        for (int j = 0; j <= MT; ++j) mg[j] = 0u;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            ge[c][0] = lm;
-#pragma unroll
-            for (int j = 1; j <= MT; ++j) ge[c][j] = 0u;
-#pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                if (i < k) {
-                    const Lmer<W> x = C.T()[S.stack_id[i] & ID_MASK];
-                    const uint32_t e = ((c & 2) ? x.h[w] : ~x.h[w]) & ((c & 1) ? x.o[w] : ~x.o[w]) & lm;
-#pragma unroll
-                    for (int j = MT; j >= 1; --j) ge[c][j] |= ge[c][j - 1] & e;
-                }
-            }
-#pragma unroll
-            for (int j = 1; j <= MT; ++j) mg[j] |= ge[c][j];
-        }
-#pragma unroll
-        for (int j = 1; j <= MT; ++j) sum_m += __popc(mg[j]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t g = 0u;
-#pragma unroll
-            for (int j = 1; j <= MT; ++j) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
-            if (C.lane == c * W + w) slot[c * W + w] = g;
-        }
-    }
-    if (C.lane == 4 * W) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - sum_m);
-    __syncwarp();
-}
-
-template <int W, int MT>
-__device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint32_t u) {
-    const uint32_t* slot = cons_slot<W, MT>(C, k);
-    const Lmer<W> x = C.T()[u & ID_MASK];
-    int matches = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const uint32_t h = x.h[w], o = x.o[w];
-        const uint32_t hit = (slot[0 * W + w] & ~h & ~o) | (slot[1 * W + w] & ~h & o) |
-                             (slot[2 * W + w] & h & ~o) | (slot[3 * W + w] & h & o);
-        matches += __popc(hit);
-    }
-    return matches >= static_cast<int>(slot[4 * W]);
-}
-
-// Next branching-row index >= it (and < end) of level k whose l-mer passes the
-// stack consensus bound, or end. The bound is evaluated for 32 consecutive
-// entries at once (one lane each) and cached as a mask, so a warp no longer
-// spends a whole loop iteration on every candidate the bound rejects (most of
-// them at t >= 5). Skipped candidates count as pushes (they are tree nodes).
-template <int W, int MT>
-__device__ __forceinline__ int next_consensus_candidate(WarpCtx<W, MT>& C, int k, int it, int end) {
-    WarpFixed& S = *C.S();
-    const LevelMeta& L = S.lev[k];
-    const uint32_t* row = level_entries<W, MT>(C, k) + L.start[L.branch];
-    const int it0 = it;
-    while (it < end) {
-        int base = S.cbase[k];
-        uint32_t mask = S.cmask[k];
-        if (base < 0 || it < base || it >= base + 32) {
-            base = it;
-            const int e = base + C.lane;
-            const bool pass = e < end && cons_check<W, MT>(C, k, row[e]);
-            mask = __ballot_sync(0xffffffffu, pass);
-            __syncwarp();
-            if (C.lane == 0) {
-                S.cbase[k] = base;
-                S.cmask[k] = mask;
-            }
-            __syncwarp();
-        }
-        const uint32_t m = mask >> (it - base);
-        if (m) {
-            it += __ffs(m) - 1;
-            break;
-        }
-        it = base + 32;
-    }
-    if (it > end) it = end;
-    C.add(W_PUSH, static_cast<unsigned long long>(it - it0));
-    return it;
-}
-
 // The same bound for the m members on the stack (u = stack[m-1] included):
 // they have a common d-neighbour only if their consensus cost is at most m*d,
 // and every deeper member can only add column cost, so a stack that fails it
@@ -1535,7 +1677,7 @@ __device__ __forceinline__ bool stack_consensus_ok(const WarpCtx<W, MT>& C, int 
     Lmer<W> Tm[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
-        if (i < m) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
+        if (i < m) Tm[i] = C.lmer(S.stack_id[i] & ID_MASK);
     return root_consensus_ok<W, MT>(C, m, Tm);
 }
 
@@ -1554,9 +1696,9 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
     Lmer<W> Tm[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
-        if (i < t) Tm[i] = C.T()[S.stack_id[i] & ID_MASK];
+        if (i < t) Tm[i] = C.lmer(S.stack_id[i] & ID_MASK);
     if constexpr (MT >= 5) {
-        if (ndon == 0 && P.prune == 2 && !root_consensus_ok<W, MT>(C, t, Tm)) {
+        if (ndon == 0 && P.prune == 2 && !P.cons_rows && !root_consensus_ok<W, MT>(C, t, Tm)) {
             C.add(W_TUPLES, 1);
             C.add(W_CLKP, static_cast<unsigned long long>(clock64() - c0));
             return;
@@ -1721,23 +1863,13 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
         S.iter_end[kmin] = it1;
     }
     __syncwarp();
-    // stack consensus bound (t >= 4 builds, pushes of a 4th+ member): the
-    // level's plurality masks are prepared once per level state (cons_prepare)
-    // and the branching row is screened 32 entries at a time
-    constexpr bool kCons = MT >= 4;
-    if constexpr (kCons) {
-        if (C.lane == 0) S.cbase[kmin] = -1;
-        __syncwarp();
-        if (kmin >= 3 && P.prune == 2) cons_prepare<W, MT>(C, kmin);
-    }
+    // (the stack consensus bound is applied by the push filters to every
+    // remaining row, so each branching-row entry already satisfies it)
     int k = kmin;
     while (k >= kmin) {
         const LevelMeta& L = S.lev[k];
-        int it = S.iter[k];
+        const int it = S.iter[k];
         const int end = S.iter_end[k];
-        if constexpr (kCons) {
-            if (k >= 3 && P.prune == 2 && it < end) it = next_consensus_candidate<W, MT>(C, k, it, end);
-        }
         if (it >= end) {
             --k;
             continue;
@@ -1759,12 +1891,8 @@ __device__ void dfs(WarpCtx<W, MT>& C, int kmin, int it0, int it1) {
             if (C.lane == 0) {
                 S.iter[k] = 0;
                 S.iter_end[k] = S.lev[k].cnt[S.lev[k].branch];
-                if constexpr (kCons) S.cbase[k] = -1;
             }
             __syncwarp();
-            if constexpr (kCons) {
-                if (k >= 3 && P.prune == 2) cons_prepare<W, MT>(C, k);
-            }
         }
     }
 }
@@ -1798,12 +1926,32 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     // allocation of the whole persistent kernel; the scanner uses it)
     Lmer<W>* T = reinterpret_cast<Lmer<W>*>(dyn_smem);
     const Lmer<W>* gT = static_cast<const Lmer<W>*>(P.table);
-    for (int i = threadIdx.x; i < P.K; i += blockDim.x) T[i] = gT[i];
-    const uint32_t table_bytes = (static_cast<uint32_t>(P.K) * sizeof(Lmer<W>) + 15u) / 16u * 16u;
-    const uint32_t wbase = table_bytes + static_cast<uint32_t>(P.plan.bytes) * warp;
-    __syncthreads();
-
     WarpCtx<W, MT> C;
+    uint32_t table_rows = static_cast<uint32_t>(P.K);
+    if constexpr (kClusterTable<W>) {
+        // this CTA's half of the table; the pair's halves are read through DSMEM
+        uint32_t rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        const uint32_t half = (static_cast<uint32_t>(P.K) + 1u) / 2u;
+        const uint32_t lo = rank * half, hi = min(static_cast<uint32_t>(P.K), lo + half);
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) T[i - lo] = gT[i];
+        const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem));
+#pragma unroll
+        for (uint32_t r = 0; r < 2; ++r)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(C.tb[r]) : "r"(local), "r"(r));
+        C.thalf = half;
+        table_rows = half;
+        // both halves staged before anyone reads across the pair
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        for (int i = threadIdx.x; i < P.K; i += blockDim.x) T[i] = gT[i];
+        C.tb[0] = C.tb[1] = 0u;
+        C.thalf = static_cast<uint32_t>(P.K);
+        __syncthreads();
+    }
+    const uint32_t table_bytes = (table_rows * static_cast<uint32_t>(sizeof(Lmer<W>)) + 15u) / 16u * 16u;
+    const uint32_t wbase = table_bytes + static_cast<uint32_t>(P.plan.bytes) * warp;
+
     C.P = &P;
     C.off_S = wbase;
     C.off_thr = wbase + P.plan.off_thr;
@@ -1815,7 +1963,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     C.node_glob = reinterpret_cast<Node<W>*>(scratch + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap);
     C.lane = lane;
     C.pushes_since_check = 0;
-    if (lane < 16) C.S()->ctr[lane] = 0;
+    if (lane < W_N) C.S()->ctr[lane] = 0;
     if (lane == 0) {
         C.S()->lazy_level = 0;
         C.S()->lazy_mask = 0u;
@@ -1827,94 +1975,18 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                                                      : static_cast<unsigned long long>(P.task_base[P.nanchors]);
     QueueState* qs = P.qs;
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
-    bool waiting = false;
-    long long wait_t0 = 0, beat_t0 = 0;
-    unsigned long long beat = 0;
-    unsigned int backoff = 128;
+    if (lane == 0) S.wait.waiting = 0;
 
     for (;;) {
         // ---- claim a task (lane 0), protocol in DESIGN.md §4
-        int kind = -1;  // -1 none, 0 static, 1 dynamic, 2 terminate
         unsigned long long idx = 0;
-        if (lane == 0) {
-            const bool have_static = statics_left(P, nstatic);
-            const unsigned long long h0 = ld_volatile(&qs->head);
-            const bool have_dyn = ld_volatile(&P.qstate[h0 % qcap]) == 2u * static_cast<unsigned int>(h0 / qcap) + 1u;
-            if (have_static || have_dyn) {
-                // announce before claiming so that no waiter can observe
-                // busy == 0 while a claimed task is still unannounced
-                atomicAdd(&qs->busy, 1u);
-                if (have_static && claim_static(P, nstatic, idx)) {
-                    kind = 0;
-                    atomicAdd(P.counters + C_STATIC, 1ull);
-                }
-                if (kind < 0) {
-                    const unsigned long long h = ld_volatile(&qs->head);
-                    if (ld_volatile(&P.qstate[h % qcap]) == 2u * static_cast<unsigned int>(h / qcap) + 1u &&
-                        atomicCAS(&qs->head, h, h + 1) == h) {
-                        kind = 1;
-                        idx = h;
-                        __threadfence();
-                    }
-                }
-                if (kind < 0) atomicSub(&qs->busy, 1u);
-            }
-            if (kind < 0) {
-                if (!waiting) {
-                    atomicAdd(&qs->waiting, 1u);
-                    waiting = true;
-                    wait_t0 = beat_t0 = clock64();
-                    beat = ld_volatile(&qs->heartbeat);
-                    backoff = 128;
-                }
-                const unsigned long long b = ld_volatile(&qs->heartbeat);
-                if (b != beat) {  // somebody is still working: not stuck
-                    beat = b;
-                    beat_t0 = clock64();
-                }
-                if (ld_volatile(&qs->busy) == 0u && ld_volatile(&qs->head) >= ld_volatile(&qs->alloc) &&
-                    !statics_left(P, nstatic)) {
-                    kind = 2;
-                } else if (clock64() - beat_t0 > (1ll << 37)) {
-                    // watchdog: ~70 s with busy warps but no heartbeat (they
-                    // beat every few starvation checks): a lost task
-                    atomicOr(P.error_flag, 8);
-                    kind = 2;
-                } else {
-                    // idle warps back off so their polling does not steal
-                    // issue slots and L2 bandwidth from the busy ones
-                    __nanosleep(backoff);
-                    backoff = min(backoff * 2, 8192u);
-                }
-            } else if (waiting) {
-                atomicSub(&qs->waiting, 1u);
-                waiting = false;
-                atomicAdd(P.counters + C_IDLE, static_cast<unsigned long long>(clock64() - wait_t0));
-            }
-        }
+        int kind = lane == 0 ? claim_task(P, nstatic, S.wait, idx) : -1;
         kind = __shfl_sync(0xffffffffu, kind, 0);
         idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (kind == 2) {
-            if (lane == 0 && waiting) {
-                atomicSub(&qs->waiting, 1u);
-                atomicAdd(P.counters + C_IDLE, static_cast<unsigned long long>(clock64() - wait_t0));
-            }
-            break;
-        }
+        if (kind == 2) break;
         if (kind < 0) continue;
-        if (P.jitter_ns && lane == 0) {
-            // schedule-shaking test hook (run_parallel's jitter, src/parallel.cpp:57-65)
-            unsigned long long z = P.jitter_seed + 0x9E3779B97F4A7C15ull * (idx + 1 + (static_cast<unsigned long long>(kind) << 40) +
-                                                                        (static_cast<unsigned long long>(gw) << 44));
-            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-            unsigned long long ns = (z ^ (z >> 31)) % (P.jitter_ns + 1);
-            while (ns > 0) {
-                const unsigned int step = static_cast<unsigned int>(ns < 1000000ull ? ns : 1000000ull);
-                __nanosleep(step);
-                ns -= step;
-            }
-        }
+        if (P.jitter_ns && lane == 0) jitter_sleep(P, idx + 1 + (static_cast<unsigned long long>(kind) << 40) +
+                                                         (static_cast<unsigned long long>(gw) << 44));
         const long long task_t0 = clock64();
         if ((P.timeline || P.log_cycles) && lane == 0) {
             // diagnostics only; kept in shared memory, not in registers
@@ -2044,9 +2116,14 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
         }
     }
     __syncwarp();
+    if constexpr (kClusterTable<W>) {
+        // the partner CTA may still read this CTA's half of the table
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     if (lane == 0) {
-        const int map[W_N] = {C_PUSHES, C_VIABLE, C_SLOTS, C_TUPLES, C_LEAVES, C_EMITTED, C_VCMP, C_NODES,
-                              C_PAIR_REJ, C_TRI_REJ, C_TASKS, C_DONATED, C_REPLAYS, C_CLK_FILTER, C_CLK_PATTERN};
+        const int map[W_N] = {C_PUSHES, C_VIABLE, C_SLOTS,    C_TUPLES,   C_LEAVES,     C_EMITTED,
+                              C_VCMP,   C_NODES,  C_PAIR_REJ, C_TRI_REJ,  C_TASKS,      C_DONATED,
+                              C_REPLAYS, C_CLK_FILTER, C_CLK_PATTERN, C_CONS_REJ};
 #pragma unroll
         for (int i = 0; i < W_N; ++i) atomicAdd(P.counters + map[i], S.ctr[i]);
     }
@@ -2088,8 +2165,11 @@ WarpPlan make_plan(int W, int l, int t) { return W == 1 ? make_plan_t<1>(l, t) :
 
 size_t node_bytes(int W) { return W == 1 ? sizeof(Node<1>) : sizeof(Node<2>); }
 
+int search_cluster(int W) { return W == 2 ? 2 : 1; }
+
 size_t search_smem(int W, int K, int warps, const WarpPlan& plan) {
-    return (static_cast<size_t>(K) * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
+    const size_t rows = (static_cast<size_t>(K) + search_cluster(W) - 1) / search_cluster(W);
+    return (rows * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
 }
 
 size_t task_slot_bytes(int W) { return (sizeof(TaskHeader) + NDON * node_bytes(W) + 127) / 128 * 128; }
@@ -2131,6 +2211,24 @@ cudaError_t set_search_smem(int W, int t, size_t bytes) {
     return cudaErrorInvalidValue;
 }
 
+// CTA pairs (2-CTA clusters) for the split two-word table
+cudaError_t launch_cluster(void (*kernel)(SearchParams), const SearchParams& P, int blocks, int warps, size_t smem,
+                           cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+    cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, P);
+}
+
 cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s) {
     const int mt = P.t < 2 ? 2 : P.t;
 #define PMS8G_CASE(WW, M)                                                 \
@@ -2141,6 +2239,7 @@ cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, s
                 return cudaGetLastError();                                \
             }                                                             \
         }                                                                 \
+        if constexpr (kClusterTable<WW>) return launch_cluster(search_kernel<WW, M, 16>, P, blocks, warps, smem, s); \
         search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P);     \
         return cudaGetLastError();                                        \
     }
