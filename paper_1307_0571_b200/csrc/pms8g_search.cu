@@ -69,6 +69,13 @@ struct WarpFixed {
     uint32_t lazy_mask;          // rows of the lazy level already filtered
     int lazy_level;              // level whose rows are filtered on demand (0: none)
     WaitState wait;              // claim loop state (lane 0)
+    // push filters of the t >= 4 builds: the older stack members, their
+    // mismatch masks against the new top and its distances to them (read by
+    // broadcast LDS in the filter loop instead of pinning ~40 registers)
+    uint32_t fsm[MAXT][4];
+    uint32_t fmiu[MAXT][2];
+    int32_t fhs[MAXT];
+    uint32_t cons[MAXT + 1][9];  // consensus row rule: slot k = masks of stack[0..k-1] (cons_prepare)
 };
 
 
@@ -128,6 +135,40 @@ struct WarpCtx {
         if (lane == 0) S()->ctr[i] += v;
     }
 };
+
+// The table location of a context in registers, for hot loops (the context
+// itself lives in local memory across the noinline calls).
+template <int W>
+struct TableRef {
+    uint32_t tb0, tb1, thalf;
+    __device__ __forceinline__ Lmer<W> get(uint32_t id) const {
+        if constexpr (kClusterTable<W>) {
+            const bool hi = id >= thalf;
+            const uint32_t addr = (hi ? tb1 : tb0) + (hi ? id - thalf : id) * static_cast<uint32_t>(sizeof(Lmer<W>));
+            uint32_t a, b, c, e;
+            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
+                         : "r"(addr));
+            Lmer<W> x;
+            x.h[0] = a;
+            x.h[W - 1] = b;
+            x.o[0] = c;
+            x.o[W - 1] = e;
+            return x;
+        } else {
+            return reinterpret_cast<const Lmer<W>*>(dyn_smem)[id];
+        }
+    }
+};
+
+template <int W, int MT>
+__device__ __forceinline__ TableRef<W> table_ref(const WarpCtx<W, MT>& C) {
+    TableRef<W> t;
+    t.tb0 = C.tb[0];
+    t.tb1 = C.tb[1];
+    t.thalf = C.thalf;
+    return t;
+}
 
 // generic (non-SWAR) enumeration tables at the start of the thr region:
 // eq[64] (members holding each symbol per position), cons[68] (consensus
@@ -235,12 +276,11 @@ __device__ __forceinline__ bool claim_static(const SearchParams& P, unsigned lon
 // computed once per push (cons_prepare, slot k); then v passes iff
 // popc(sum over c of G[c] & [v == c]) >= need (adding v raises a column's
 // maximum exactly where v holds a plurality symbol). Kept in the warp's
-// global scratch, 4W+1 words per slot.
+// shared memory (read by broadcast LDS in the filter loops), 4W+1 words per
+// slot.
 template <int W, int MT>
 __device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
-    const SearchParams& P = *C.P;
-    return C.lvl_glob + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap +
-           static_cast<size_t>(P.node_cap) * (sizeof(Node<W>) / 4) + 9 * k;
+    return C.S()->cons[k];
 }
 
 template <int W, int MT>
@@ -304,35 +344,29 @@ __device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint3
     return matches >= static_cast<int>(slot[4 * W]);
 }
 
-// The slot's masks hoisted into registers for a filter pass.
+// A view of one slot for a filter pass (the masks stay in shared memory:
+// pinned in registers they would be spilled around the filter loop).
 template <int W>
 struct ConsMasks {
-    uint32_t g[4][W];
-    int need;
+    const uint32_t* slot;
 };
 
 template <int W, int MT>
 __device__ __forceinline__ ConsMasks<W> load_cons(const WarpCtx<W, MT>& C, int k) {
-    const uint32_t* slot = cons_slot<W, MT>(C, k);
-    ConsMasks<W> cm;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int w = 0; w < W; ++w) cm.g[c][w] = slot[c * W + w];
-    cm.need = static_cast<int>(slot[4 * W]);
-    return cm;
+    return ConsMasks<W>{cons_slot<W, MT>(C, k)};
 }
 
 template <int W>
 __device__ __forceinline__ bool cons_pass(const ConsMasks<W>& cm, const Lmer<W>& x) {
+    const uint32_t* g = cm.slot;
     int matches = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
         const uint32_t h = x.h[w], o = x.o[w];
-        matches += __popc((cm.g[0][w] & ~(h | o)) | (cm.g[1][w] & o & ~h) | (cm.g[2][w] & h & ~o) |
-                          (cm.g[3][w] & h & o));
+        matches += __popc((g[0 * W + w] & ~(h | o)) | (g[1 * W + w] & o & ~h) | (g[2 * W + w] & h & ~o) |
+                          (g[3 * W + w] & h & o));
     }
-    return matches >= cm.need;
+    return matches >= static_cast<int>(g[4 * W]);
 }
 
 // Pushes whose filter applies the consensus row rule: stack + v has 4+
@@ -407,6 +441,76 @@ __device__ __noinline__ int claim_task(const SearchParams& P, unsigned long long
     return kind;
 }
 
+// The older stack members s_i (i < k) of a push of u = stack[k], for the
+// Theorem-1 triple rule: Hd(v, s_i), Hd(s_i, u) and the all-distinct count
+// n4 = popc(mism(v,s_i) & mism(v,u) & mism(s_i,u)) give the triple's
+// consensus cost Cd3 = (h_vi + h_vu + h_iu + n4) / 2 <= 3d
+// (MotifSearch::push, src/solver.cpp:302-319, with its sum + min <= 6d
+// shortcut). Builds with t <= 3 keep the members in registers; t >= 4 builds
+// keep them in shared memory (broadcast reads; most slots never get here).
+template <int W, int MT>
+struct StackSet {
+    static constexpr bool kSmem = MT >= 4;
+    Lmer<W> sm[kSmem ? 1 : MT];
+    Mask<W> miu[kSmem ? 1 : MT];
+    int hs[kSmem ? 1 : MT];
+    const WarpFixed* S;
+
+    __device__ __forceinline__ void load(const WarpCtx<W, MT>& C, int k, const Lmer<W>& U) {
+        const TableRef<W> tr = table_ref<W, MT>(C);
+        WarpFixed* Sw = C.S();
+        S = Sw;
+        if constexpr (kSmem) {
+            if (C.lane < k) {
+                const Lmer<W> x = tr.get(Sw->stack_id[C.lane] & ID_MASK);
+                const Mask<W> m = mism<W>(x, U);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    Sw->fsm[C.lane][2 * w] = x.h[w];
+                    Sw->fsm[C.lane][2 * w + 1] = x.o[w];
+                    Sw->fmiu[C.lane][w] = m.w[w];
+                }
+                Sw->fhs[C.lane] = popcm<W>(m);
+            }
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < k) {
+                    sm[i] = tr.get(Sw->stack_id[i] & ID_MASK);
+                    miu[i] = mism<W>(sm[i], U);
+                    hs[i] = popcm<W>(miu[i]);
+                }
+        }
+    }
+
+    __device__ __forceinline__ bool triple_ok(int i, const Lmer<W>& V, const Mask<W>& mu, int hvu,
+                                              int six_d) const {
+        Lmer<W> x;
+        Mask<W> mi_u;
+        int h_iu;
+        if constexpr (kSmem) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                x.h[w] = S->fsm[i][2 * w];
+                x.o[w] = S->fsm[i][2 * w + 1];
+                mi_u.w[w] = S->fmiu[i][w];
+            }
+            h_iu = S->fhs[i];
+        } else {
+            x = sm[i];
+            mi_u = miu[i];
+            h_iu = hs[i];
+        }
+        const Mask<W> mi = mism<W>(V, x);
+        const int hvi = popcm<W>(mi);
+        const int sum = hvi + hvu + h_iu;
+        if (sum > six_d) return false;
+        const int mn = min(min(hvi, hvu), h_iu);
+        return sum + mn <= six_d || sum + popc_and3<W>(mi, mu, mi_u) <= six_d;
+    }
+};
+
 // ---------------------------------------------------------------- push filter
 // Push of u = stack[k] onto a stack of k members: filter level k (minus its
 // branching row) into level k+1. Returns viable (no remaining row emptied).
@@ -422,18 +526,10 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const int d = P.d, six_d = 6 * d, two_d = 2 * d;
     const long long f0 = clock64();
 
-    const Lmer<W> U = C.lmer(S.stack_id[k] & ID_MASK);
-    Lmer<W> Sm[MT];
-    Mask<W> Miu[MT];
-    int hs[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        if (i < k) {
-            Sm[i] = C.lmer(S.stack_id[i] & ID_MASK);
-            Miu[i] = mism<W>(Sm[i], U);
-            hs[i] = popcm<W>(Miu[i]);
-        }
-    }
+    const TableRef<W> tr = table_ref<W, MT>(C);
+    const Lmer<W> U = tr.get(S.stack_id[k] & ID_MASK);
+    StackSet<W, MT> ss;
+    ss.load(C, k, U);
     const bool cons = cons_rows_at<MT>(P, k);
     ConsMasks<W> cm;
     if (cons) {
@@ -462,27 +558,25 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         e_next = load_entry(f + 32);
         bool keep = false;
         if (valid) {
-            const Lmer<W> V = C.lmer(e & ID_MASK);
-            const Mask<W> mu = mism<W>(V, U);
-            const int hvu = popcm<W>(mu);
-            keep = hvu <= two_d;
-            pair_rej += !keep;
-            if (cons && keep) {
+            const Lmer<W> V = tr.get(e & ID_MASK);
+            // the consensus rule first: at deep levels it rejects most slots
+            keep = true;
+            if (cons) {
                 keep = cons_pass<W>(cm, V);
                 cons_rej += !keep;
+            }
+            Mask<W> mu;
+            int hvu = 0;
+            if (keep) {
+                mu = mism<W>(V, U);
+                hvu = popcm<W>(mu);
+                keep = hvu <= two_d;
+                pair_rej += !keep;
             }
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 if (i < k && keep) {
-                    const Mask<W> mi = mism<W>(V, Sm[i]);
-                    const int hvi = popcm<W>(mi);
-                    const int sum = hvi + hvu + hs[i];
-                    if (sum > six_d) {
-                        keep = false;
-                    } else {
-                        const int mn = min(min(hvi, hvu), hs[i]);
-                        if (sum + mn > six_d) keep = sum + popc_and3<W>(mi, mu, Miu[i]) <= six_d;
-                    }
+                    keep = ss.triple_ok(i, V, mu, hvu, six_d);
                     tri_rej += !keep;
                 }
             }
@@ -575,18 +669,10 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     const bool cons = cons_rows_at<MT>(P, k);
     ConsMasks<W> cm;
     if (cons) cm = load_cons<W, MT>(C, k + 1);
-    const Lmer<W> U = C.lmer(S.stack_id[k] & ID_MASK);
-    Lmer<W> Sm[MT];
-    Mask<W> Miu[MT];
-    int hs[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        if (i < k) {
-            Sm[i] = C.lmer(S.stack_id[i] & ID_MASK);
-            Miu[i] = mism<W>(Sm[i], U);
-            hs[i] = popcm<W>(Miu[i]);
-        }
-    }
+    const TableRef<W> tr = table_ref<W, MT>(C);
+    const Lmer<W> U = tr.get(S.stack_id[k] & ID_MASK);
+    StackSet<W, MT> ss;
+    ss.load(C, k, U);
     int out = 0;
     uint32_t e_next = lane < cnt ? src[lane] : 0u;  // one block ahead
     for (int base = 0; base < cnt; base += 32) {
@@ -595,21 +681,18 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
         const uint32_t e = e_next;
         e_next = f + 32 < cnt ? src[f + 32] : 0u;
         if (f < cnt) {
-            const Lmer<W> V = C.lmer(e & ID_MASK);
-            const Mask<W> mu = mism<W>(V, U);
-            const int hvu = popcm<W>(mu);
-            keep = hvu <= two_d;
-            if (cons && keep) keep = cons_pass<W>(cm, V);
-#pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                if (i < k && keep) {
-                    const Mask<W> mi = mism<W>(V, Sm[i]);
-                    const int hvi = popcm<W>(mi);
-                    const int sum = hvi + hvu + hs[i];
-                    const int mn = min(min(hvi, hvu), hs[i]);
-                    keep = sum <= six_d && (sum + mn <= six_d || sum + popc_and3<W>(mi, mu, Miu[i]) <= six_d);
-                }
+            const Lmer<W> V = tr.get(e & ID_MASK);
+            keep = !cons || cons_pass<W>(cm, V);
+            Mask<W> mu;
+            int hvu = 0;
+            if (keep) {
+                mu = mism<W>(V, U);
+                hvu = popcm<W>(mu);
+                keep = hvu <= two_d;
             }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                if (i < k && keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (keep) dst[out + __popc(bal & lanemask_lt())] = e;

@@ -69,6 +69,41 @@ def test_anchor_sample_23_9():
     _anchor_parity("anchors_23_9.json", 23, 9)
 
 
+def test_full_instance_21_8_against_every_reference_anchor():
+    # tests/golden/anchors_21_8_full.json: the reference's run_anchored motif
+    # set of EVERY S1 l-mer of (21,8) seed 1 (make_golden.py heavy21full); the
+    # whole-instance GPU answer must be their union (run_parallel,
+    # src/parallel.cpp:88-90), and a spread of single S1 l-mers (including
+    # the non-empty one) must match one by one
+    g = golden("anchors_21_8_full.json")
+    assert len(g["anchors"]) == 580
+    inst = planted(21, 8, g["seed"])
+    union = sorted({m for a in g["anchors"] for m in a["motifs"]})
+    assert union and inst.motif in union
+    assert P.solve(inst.problem) == union
+    nonempty = [a for a in g["anchors"] if a["motifs"]]
+    sample = nonempty + g["anchors"][::29]
+    for a in sample:
+        got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=[a["offset"]]))
+        assert got == a["motifs"], a["offset"]
+    # several S1 l-mers in one call: the union of theirs
+    offs = [a["offset"] for a in sample]
+    want = sorted({m for a in sample for m in a["motifs"]})
+    assert P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=offs)) == want
+
+
+@pytest.mark.parametrize("l,d,n,m,seed", [(34, 10, 6, 60, 1), (38, 11, 6, 60, 2), (45, 13, 5, 60, 6),
+                                          (28, 9, 6, 50, 7), (24, 8, 6, 60, 5)])
+def test_deep_switch_depths_against_oracle(l, d, n, m, seed):
+    # the t >= 4 builds (consensus row rule, stack bound, 5/6-member tuples) on
+    # one- and two-word l-mers, every t against the complete C oracle
+    inst = planted(l, d, seed, n=n, m=m)
+    want, _ = O.solve(inst.codes, l, d)
+    assert inst.motif in want
+    for t in range(2, min(n, 6) + 1):
+        assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == want, t
+
+
 def test_small_random_and_edge_cases():
     for case in golden("small_random.json"):
         prob = P.Problem(case["sequences"], case["l"], case["d"])
