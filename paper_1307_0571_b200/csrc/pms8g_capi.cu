@@ -1155,6 +1155,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
         // the consensus row rule changes the tree (not the motif set): off for exact_tree
         P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
+        if (P.cons_rows && std::getenv("PMS8G_CONS3")) P.cons_rows |= 2;  // also the t = 3 lazy rows (experiment)
         P.plan = c->plan;
         P.scratch = c->d_scratch;
         P.scratch_words = c->scratch_words;
@@ -1165,6 +1166,10 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         P.key_cap = c->key_cap;
         P.counters = c->d_counters;
         P.error_flag = c->d_err;
+        // cross-GPU claims: 4 tasks per NVLink CAS until the last 16 per warp of this device
+        P.claim_chunk = 4;
+        if (const char* e = std::getenv("PMS8G_CLAIM_CHUNK")) P.claim_chunk = std::max(1, std::atoi(e));
+        P.chunk_until = 16ll * c->blocks * c->warps;
         P.jitter_ns = 1000ull * c->opt.jitter_max_us;
         P.jitter_seed = c->opt.jitter_seed;
         P.gqueue = nullptr;

@@ -53,6 +53,7 @@ struct WaitState {
     unsigned int backoff;
     long long wait_t0, beat_t0;
     unsigned long long beat;
+    unsigned long long chunk_next, chunk_end;  // static tasks claimed in a chunk, not yet started
 };
 
 struct WarpFixed {
@@ -239,25 +240,32 @@ __device__ __forceinline__ bool statics_left(const SearchParams& P, unsigned lon
     return ep < P.gepoch || (ep == P.gepoch && (v & GQ_MASK) < nstatic);
 }
 
+// Claims static tasks [idx, idx + n). From the shared cross-GPU counter a
+// warp takes a chunk of up to P.claim_chunk tasks per CAS while more than
+// P.chunk_until tasks remain (far from the tail, where imbalance costs
+// nothing and every CAS is an NVLink round trip), then one at a time.
 __device__ __forceinline__ bool claim_static(const SearchParams& P, unsigned long long nstatic,
-                                             unsigned long long& idx) {
+                                             unsigned long long& idx, unsigned int& n) {
+    n = 1;
     if (!P.gqueue) {
         idx = atomicAdd(&P.qs->static_next, 1ull);
         return idx < nstatic;
     }
     unsigned long long v = ld_relaxed_sys(P.gqueue);
     for (;;) {
-        const unsigned long long ep = v >> GQ_SHIFT, cnt = v & GQ_MASK;
-        unsigned long long nv;
+        const unsigned long long ep = v >> GQ_SHIFT;
+        unsigned long long cnt = v & GQ_MASK, nv;
         if (ep > P.gepoch) return false;
         if (ep < P.gepoch) {
-            nv = (P.gepoch << GQ_SHIFT) | 1ull;
-            idx = 0;
-        } else {
-            if (cnt >= nstatic) return false;
-            nv = v + 1ull;
-            idx = cnt;
+            cnt = 0;  // this run's epoch opens at task 0
+        } else if (cnt >= nstatic) {
+            return false;
         }
+        const unsigned long long left = nstatic - cnt;
+        n = left > static_cast<unsigned long long>(P.chunk_until) ? static_cast<unsigned int>(P.claim_chunk) : 1u;
+        if (n > left) n = static_cast<unsigned int>(left);
+        nv = (P.gepoch << GQ_SHIFT) | (cnt + n);
+        idx = cnt;
         const unsigned long long old = atomicCAS_system(P.gqueue, v, nv);
         if (old == v) return true;
         v = old;
@@ -373,7 +381,7 @@ __device__ __forceinline__ bool cons_pass(const ConsMasks<W>& cm, const Lmer<W>&
 // members (k >= 2), full pruning, t >= 4 builds.
 template <int MT>
 __device__ __forceinline__ bool cons_rows_at(const SearchParams& P, int k) {
-    return MT >= 4 && P.cons_rows && k >= 2;
+    return (MT >= 4 || (MT == 3 && (P.cons_rows & 2))) && (P.cons_rows & 1) && k >= 2;
 }
 
 // One claim attempt by lane 0: 0 static task, 1 dynamic task (idx set),
@@ -383,6 +391,11 @@ __device__ __noinline__ int claim_task(const SearchParams& P, unsigned long long
     QueueState* qs = P.qs;
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
     int kind = -1;
+    if (ws.chunk_next < ws.chunk_end) {
+        // the rest of this warp's claimed chunk (already counted as busy)
+        idx = ws.chunk_next++;
+        return 0;
+    }
     const bool have_static = statics_left(P, nstatic);
     const unsigned long long h0 = ld_volatile(&qs->head);
     const bool have_dyn = ld_volatile(&P.qstate[h0 % qcap]) == 2u * static_cast<unsigned int>(h0 / qcap) + 1u;
@@ -390,9 +403,16 @@ __device__ __noinline__ int claim_task(const SearchParams& P, unsigned long long
         // announce before claiming so that no waiter can observe
         // busy == 0 while a claimed task is still unannounced
         atomicAdd(&qs->busy, 1u);
-        if (have_static && claim_static(P, nstatic, idx)) {
+        unsigned int n = 1;
+        if (have_static && claim_static(P, nstatic, idx, n)) {
             kind = 0;
-            atomicAdd(P.counters + C_STATIC, 1ull);
+            atomicAdd(P.counters + C_STATIC, static_cast<unsigned long long>(n));
+            if (n > 1) {
+                // the chunk's later tasks stay announced until they are done
+                atomicAdd(&qs->busy, n - 1);
+                ws.chunk_next = idx + 1;
+                ws.chunk_end = idx + n;
+            }
         }
         if (kind < 0) {
             const unsigned long long h = ld_volatile(&qs->head);
@@ -550,15 +570,21 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     auto load_entry = [&](int f) -> uint32_t {
         return f < n_iter ? src[f < bstart ? f : f + bcnt] : 0xFFFFFFFFu;
     };
+    // software pipeline: entries two blocks ahead, their l-mers (table reads,
+    // DSMEM for two-word l-mers) one block ahead
     uint32_t e_next = load_entry(lane);
+    uint32_t e_next2 = load_entry(lane + 32);
+    Lmer<W> V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
     for (int base = 0; base < n_iter; base += 32) {
         const int f = base + lane;
         const bool valid = f < n_iter;
         const uint32_t e = e_next;
-        e_next = load_entry(f + 32);
+        const Lmer<W> V = V_next;
+        e_next = e_next2;
+        e_next2 = load_entry(f + 64);
+        if (base + 32 < n_iter) V_next = tr.get(f + 32 < n_iter ? e_next & ID_MASK : 0u);
         bool keep = false;
         if (valid) {
-            const Lmer<W> V = tr.get(e & ID_MASK);
             // the consensus rule first: at deep levels it rejects most slots
             keep = true;
             if (cons) {
@@ -674,14 +700,19 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     StackSet<W, MT> ss;
     ss.load(C, k, U);
     int out = 0;
-    uint32_t e_next = lane < cnt ? src[lane] : 0u;  // one block ahead
+    // entries two blocks ahead, their l-mers one block ahead (as filter_push)
+    uint32_t e_next = lane < cnt ? src[lane] : 0u;
+    uint32_t e_next2 = lane + 32 < cnt ? src[lane + 32] : 0u;
+    Lmer<W> V_next = tr.get(e_next & ID_MASK);
     for (int base = 0; base < cnt; base += 32) {
         const int f = base + lane;
         bool keep = false;
         const uint32_t e = e_next;
-        e_next = f + 32 < cnt ? src[f + 32] : 0u;
+        const Lmer<W> V = V_next;
+        e_next = e_next2;
+        e_next2 = f + 64 < cnt ? src[f + 64] : 0u;
+        if (base + 32 < cnt) V_next = tr.get(e_next & ID_MASK);
         if (f < cnt) {
-            const Lmer<W> V = tr.get(e & ID_MASK);
             keep = !cons || cons_pass<W>(cm, V);
             Mask<W> mu;
             int hvu = 0;
@@ -2058,7 +2089,10 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                                                      : static_cast<unsigned long long>(P.task_base[P.nanchors]);
     QueueState* qs = P.qs;
     const unsigned long long qcap = static_cast<unsigned long long>(P.qcap);
-    if (lane == 0) S.wait.waiting = 0;
+    if (lane == 0) {
+        S.wait.waiting = 0;
+        S.wait.chunk_next = S.wait.chunk_end = 0;
+    }
 
     for (;;) {
         // ---- claim a task (lane 0), protocol in DESIGN.md §4
