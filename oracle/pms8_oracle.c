@@ -345,30 +345,31 @@ int64_t pms8o_common_neighborhood(const uint8_t* tuple, int k, int l, int sigma,
     return e.visited;
 }
 
-/* ---- packed l-mers: 2-bit symbols, 32 per 64-bit word, LSB-first
- *      (PackedSequenceSet / hamming64_*, include/pms8/packed_seq.hpp:79-170;
- *      the reference uses 28-symbol chunks, the distance is the same) ---- */
+/* ---- packed l-mers: 5 bit planes of one 64-bit word (l <= 64, codes < 32):
+ *      bit p of plane k = bit k of the code at position p. Hamming distance is
+ *      popcount(OR_k plane_k(a) ^ plane_k(b)), for DNA exactly the reference's
+ *      group-folded 2-bit distance (hamming64_*, include/pms8/packed_seq.hpp:
+ *      127-170) and for b-bit alphabets its b-bit groups
+ *      (src/alphabet.cpp:41). `words` is always 1 here. ---- */
 typedef struct {
-    uint64_t w[2];
+    uint64_t pl[5];
 } pk;
 
-static inline int pk_dist(const pk* a, const pk* b, int words) {
-    int dist = 0;
-    for (int i = 0; i < words; ++i) {
-        const uint64_t x = a->w[i] ^ b->w[i];
-        dist += __builtin_popcountll((x | (x >> 1)) & 0x5555555555555555ULL);
-    }
-    return dist;
+static inline uint64_t pk_fold(const pk* a, const pk* b, int i) {
+    (void)i;
+    return (a->pl[0] ^ b->pl[0]) | (a->pl[1] ^ b->pl[1]) | (a->pl[2] ^ b->pl[2]) | (a->pl[3] ^ b->pl[3]) |
+           (a->pl[4] ^ b->pl[4]);
 }
 
-static inline uint64_t pk_fold(const pk* a, const pk* b, int i) {
-    const uint64_t x = a->w[i] ^ b->w[i];
-    return (x | (x >> 1)) & 0x5555555555555555ULL;
+static inline int pk_dist(const pk* a, const pk* b, int words) {
+    (void)words;
+    return __builtin_popcountll(pk_fold(a, b, 0));
 }
 
 static void pk_pack(const uint8_t* codes, int l, pk* out) {
-    out->w[0] = out->w[1] = 0;
-    for (int p = 0; p < l; ++p) out->w[p >> 5] |= (uint64_t)codes[p] << (2 * (p & 31));
+    for (int k = 0; k < 5; ++k) out->pl[k] = 0;
+    for (int p = 0; p < l; ++p)
+        for (int k = 0; k < 5; ++k) out->pl[k] |= (uint64_t)((codes[p] >> k) & 1u) << p;
 }
 
 /* ---- the search: RowMatrix + MotifSearch (src/solver.cpp:156-432) ---- */
@@ -589,7 +590,7 @@ static int64_t canonical(uint8_t* raw, int64_t nraw, int l) {
 
 int64_t pms8o_solve(const uint8_t* codes, int n, int m, int l, int d, int sigma, int t, const int32_t* anchors,
                     int nanchors, uint8_t* out, int64_t cap, int64_t* counters) {
-    if (n < 1 || l < 1 || l > m || d < 0 || d > l || l > 64 || sigma > 4) return -1;
+    if (n < 1 || l < 1 || l > m || d < 0 || d > l || l > 64 || sigma < 2 || sigma > 32) return -1;
     search_t s;
     memset(&s, 0, sizeof s);
     s.n = n;
@@ -601,7 +602,7 @@ int64_t pms8o_solve(const uint8_t* codes, int n, int m, int l, int d, int sigma,
     if (s.t < 1 || s.t > n || s.t > PMS8O_MAX_K) return -1;
     s.w = m - l + 1;
     s.K = (int64_t)n * s.w;
-    s.words = (l + 31) / 32;
+    s.words = 1; /* one 64-bit word per bit plane */
     s.codes = codes;
     s.lmers = (pk*)malloc(sizeof(pk) * (size_t)s.K);
     for (int r = 0; r < n; ++r)

@@ -15,7 +15,7 @@
 //   canonical_motif_set        src/solver.cpp:16-21
 //
 // Sub-commands (all print to stdout; numbers are plain text or one JSON line):
-//   gen    l d seed [n m mode]             -> motif, positions, sequences
+//   gen    l d seed [n m mode alphabet]    -> motif, positions, sequences
 //   solve  l d seed threads [t]            -> sorted motif set of run_parallel + report
 //   anchors l d seed threads "o1,o2,.." [t] -> per-anchor sorted motif sets (run_anchored)
 //   time   l d seed threads stride [t]     -> ctx build + strided anchors, timing JSON
@@ -23,7 +23,7 @@
 //   stats  l d seed "o1,.." [t]            -> per-depth work counters (mirrors recurse())
 //   branchtime l d seed threads jobs cap [t] -> capped depth-1 branch sample (CPU baseline, (50,21))
 //   kat                                    -> SPEC known-answer values as JSON
-//   file   path l d threads [t]            -> solve sequences read from a file (one per line)
+//   file   path l d threads [t alphabet]   -> solve sequences read from a file (one per line)
 #include <omp.h>
 
 #include <algorithm>
@@ -79,8 +79,10 @@ std::vector<long> parse_list(const std::string& s) {
     return out;
 }
 
-PlantedInstance make(int l, int d, uint64_t seed, int n = 20, int m = 600, bool exact = true) {
+PlantedInstance make(int l, int d, uint64_t seed, int n = 20, int m = 600, bool exact = true,
+                     const std::string& alphabet = "dna") {
     PlantedInstanceSpec spec;
+    spec.alphabet = Alphabet::named(alphabet);
     spec.l = l;
     spec.d = d;
     spec.n = n;
@@ -158,7 +160,8 @@ int cmd_gen(int argc, char** argv) {
     const int n = argc > 5 ? std::atoi(argv[5]) : 20;
     const int m = argc > 6 ? std::atoi(argv[6]) : 600;
     const bool exact = argc > 7 ? std::string(argv[7]) == "exact" : true;
-    const auto inst = make(l, d, seed, n, m, exact);
+    const std::string alphabet = argc > 8 ? argv[8] : "dna";
+    const auto inst = make(l, d, seed, n, m, exact, alphabet);
     std::printf("MOTIF %s\nPOSITIONS", inst.motif.c_str());
     for (int p : inst.positions) std::printf(" %d", p);
     std::printf("\n");
@@ -193,6 +196,7 @@ int cmd_file(int argc, char** argv) {
     problem.max_mismatches = std::atoi(argv[4]);
     const int threads = std::atoi(argv[5]);
     const int t = argc > 6 ? std::atoi(argv[6]) : 0;
+    if (argc > 7) problem.alphabet = Alphabet::named(argv[7]);
     return solve_and_print(problem, threads, t);
 }
 

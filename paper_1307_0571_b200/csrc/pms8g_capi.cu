@@ -27,6 +27,7 @@
 #include "pms8g_device.cuh"
 #include "pms8g_internal.h"
 #include "pms8g_launch.h"
+#include "pms8g_sigma.h"
 
 using namespace pms8g;
 
@@ -58,6 +59,9 @@ unsigned __int128 nsize(int l, int d, int sigma) {
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
     int ref_t = 0;  // the reference's switch depth (override or estimate_threshold), reported
+    int B = 2;          // bits (planes) per symbol: 2 for sigma <= 4 (two-plane DNA path), else ceil(log2 sigma)
+    bool sig = false;   // sigma > 4: the B-plane search (pms8g_sigma.cu)
+    int key_bits() const { return B * l; }
     std::string alphabet;
     pms8g_options opt{};
     std::vector<int32_t> anchors;
@@ -191,7 +195,7 @@ int ensure_key_capacity(pms8g_ctx* c, long long need, char* err, size_t errlen) 
     using K128 = unsigned __int128;
     cub::DeviceRadixSort::SortKeys(nullptr, b1, reinterpret_cast<K128*>(c->d_keys),
                                    reinterpret_cast<K128*>(c->d_keys_sorted), static_cast<int>(cap), 0,
-                                   std::max(1, 2 * c->l));
+                                   std::max(1, c->key_bits()));
     cub::DeviceSelect::Unique(nullptr, b2, reinterpret_cast<K128*>(c->d_keys_sorted),
                               reinterpret_cast<K128*>(c->d_keys_unique), c->d_unique_count, static_cast<int>(cap));
     c->cub_bytes = std::max(b1, b2);
@@ -212,11 +216,21 @@ int validate_problem(int n, int m, int l, int d, const char* alphabet, char* err
         for (int j = 0; j < i; ++j)
             if (alphabet[i] == alphabet[j])
                 return fail(err, errlen, PMS8G_ERR_INVALID, "duplicate alphabet symbol '%c'", alphabet[i]);
-    // GPU path limits: 2 bit planes, 32 rows per warp table,
-    // 24-bit l-mer ids, 16-bit row offsets
-    if (s > 4)
-        return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 4 symbols, got %d", s);
-    if (l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
+    // GPU path limits: 2 bit planes up to 4 symbols (l <= 64),
+    // B = ceil(log2 sigma) planes of one word up to 32 symbols (l <= 32 and
+    // B*l <= 128 key bits), 32 rows per warp table, 24-bit l-mer ids, 16-bit
+    // row offsets
+    if (s > 32)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 32 symbols, got %d", s);
+    if (s <= 4 && l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
+    if (s > 4) {
+        const int b = sigma_planes(s);
+        const int lmax = std::min(32, 128 / b);
+        if (l > lmax)
+            return fail(err, errlen, PMS8G_ERR_INVALID,
+                        "GPU path supports l <= %d for a %d-symbol alphabet (%d bits per symbol), got %d", lmax, s, b,
+                        l);
+    }
     if (n > MAXN) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n <= %d sequences, got %d", MAXN, n);
     const long long K = static_cast<long long>(n) * (m - l + 1);
     if (K > 65535) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n*(m-l+1) <= 65535, got %lld", K);
@@ -461,6 +475,13 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     c->sigma = sigma;
     c->alphabet = alphabet ? alphabet : "ACGT";
     c->W = l <= 32 ? 1 : 2;
+    c->sig = sigma > 4;
+    c->B = c->sig ? sigma_planes(sigma) : 2;
+    if (c->sig && (opt.queue || (opt.branches && opt.nbranches > 0))) {
+        delete c;
+        return fail(err, errlen, PMS8G_ERR_INVALID,
+                    "shared queues and explicit branches need an alphabet of at most 4 symbols");
+    }
     c->w = m - l + 1;
     c->K = n * c->w;
     c->t = t;
@@ -520,27 +541,37 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     // launch shape: one persistent block per SM, as many warps as the
     // shared-memory l-mer table leaves room for
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
-    c->plan = make_plan(c->W, l, t);
-    int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
-    while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap) --warps;  // + static smem (TMA barrier)
-    if (search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap)
-        return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
-                                 "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K, smem_cap));
-    c->warps = warps;
-    c->smem = search_smem(c->W, c->K, warps, c->plan);
-    c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
-    // clusters of search_cluster(W) CTAs share the l-mer table: whole clusters only
-    const int cs = search_cluster(c->W);
-    c->blocks = std::max(cs, c->blocks / cs * cs);
-    if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
-        return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
+    if (c->sig) {
+        // sigma-symbol search: table in global memory (L1/L2), per-warp state in shared memory
+        c->warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : 16;
+        c->smem = sigma_warp_smem() * c->warps;
+        c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
+    } else {
+        c->plan = make_plan(c->W, l, t);
+        int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
+        while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap) --warps;  // + static smem
+        if (search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap)
+            return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
+                                     "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K,
+                                     smem_cap));
+        c->warps = warps;
+        c->smem = search_smem(c->W, c->K, warps, c->plan);
+        c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
+        // clusters of search_cluster(W) CTAs share the l-mer table: whole clusters only
+        const int cs = search_cluster(c->W);
+        c->blocks = std::max(cs, c->blocks / cs * cs);
+        if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
+            return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
+    }
+    const int warps = c->warps;
 
     const int na = static_cast<int>(c->anchors.size());
     c->level_cap = (c->K + 31) / 32 * 32;  // keeps the per-warp node overflow 16-byte aligned
     c->node_cap = 64 * (l + 4);
     if (const char* e = std::getenv("PMS8G_NODE_CAP")) c->node_cap = std::max(0, std::atoi(e));  // failure tests
     const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
-    const size_t node_words = static_cast<size_t>(c->node_cap) * node_bytes(c->W) / 4;
+    const size_t node_words =
+        static_cast<size_t>(c->node_cap) * (c->sig ? sigma_node_bytes() : node_bytes(c->W)) / 4;
     c->scratch_words = (lvl_words + node_words + 64 + 31) / 32 * 32;  // + consensus masks (cons_slot)
     const size_t nwarps_total = static_cast<size_t>(c->blocks) * warps;
     int rc2;
@@ -548,7 +579,8 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     if ((rc2 = alloc(c, reinterpret_cast<void**>(&(ptr)), (bytes), err, errlen)) != PMS8G_OK) \
         return cleanup_fail(rc2);
     AL(c->d_codes, static_cast<size_t>(n) * m);
-    AL(c->d_table, (static_cast<size_t>(c->K) * lmer_bytes(c->W) + 15) / 16 * 16);  // TMA-staged: 16-byte multiple
+    AL(c->d_table, (static_cast<size_t>(c->K) * (c->sig ? sigma_lmer_bytes(c->B) : lmer_bytes(c->W)) + 15) / 16 *
+                       16);  // 16-byte multiple (bulk-copy staging)
     AL(c->d_anchors, sizeof(int32_t) * std::max(1, na));
     AL(c->d_l1, sizeof(uint32_t) * static_cast<size_t>(std::max(1, na)) * c->K);
     AL(c->d_meta, sizeof(LevelMeta) * std::max(1, na));
@@ -561,7 +593,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     AL(c->d_err, 2 * sizeof(int));  // flags, failing S1 offset + 1
     AL(c->d_task_ai, sizeof(int32_t) * std::max<size_t>(1, c->task_ai.size()));
     AL(c->d_task_u, sizeof(uint32_t) * std::max<size_t>(1, c->task_u.size()));
-    if (c->task_u.empty() && t >= 2 && !std::getenv("PMS8G_NO_TASK_ORDER")) {
+    if (c->task_u.empty() && t >= 2 && !c->sig && !std::getenv("PMS8G_NO_TASK_ORDER")) {
         // heaviest-first static task order (taskorder_kernel + stable radix sort)
         c->order_cap = static_cast<long long>(std::max(1, na)) * c->w;
         AL(c->d_order, sizeof(uint32_t) * 4 * c->order_cap);
@@ -661,12 +693,17 @@ int pms8g_ctx_kernel_ms(pms8g_ctx* c, float* search_ms, float* rowbuild_ms) {
 
 void pms8g_decode_keys(const uint64_t* keys, int64_t count, int l, const char* alphabet, char* out) {
     const char* sym = alphabet ? alphabet : "ACGT";
+    // bits per symbol: 2 up to 4 symbols, else ceil(log2 sigma) (the B-plane path)
+    const int sigma = static_cast<int>(std::strlen(sym));
+    const int b = sigma <= 4 ? 2 : sigma_planes(sigma);
+    const uint64_t mask = (1ull << b) - 1ull;
     for (int64_t i = 0; i < count; ++i) {
         const uint64_t lo = keys[2 * i], hi = keys[2 * i + 1];
         for (int p = 0; p < l; ++p) {
-            const int sh = 2 * (l - 1 - p);
-            const int code = static_cast<int>(((sh >= 64) ? (hi >> (sh - 64)) : (lo >> sh)) & 3u);
-            out[i * l + p] = sym[code];
+            const int sh = b * (l - 1 - p);
+            uint64_t v = sh >= 64 ? (hi >> (sh - 64)) : (lo >> sh);
+            if (sh < 64 && sh + b > 64) v |= hi << (64 - sh);
+            out[i * l + p] = sym[static_cast<int>(v & mask)];
         }
     }
     // keys sort in code order; canonical_motif_set (src/solver.cpp:16-21)
@@ -1101,101 +1138,141 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         CU(cudaMemsetAsync(c->d_qstate, 0, sizeof(unsigned int) * c->qcap, s));
         CU(cudaMemsetAsync(c->d_err, 0, 2 * sizeof(int), s));
         CU(cudaMemsetAsync(c->d_fail, 0, sizeof(int), s));
-        CU(launch_encode(c->W, c->d_codes, c->n, c->m, c->l, c->w, c->d_table, c->d_err, s));
-        CU(cudaEventRecord(c->ev[0], s));
-        CU(launch_rowbuild(c->W, c->d_table, c->n, c->w, c->d, c->K, c->opt.sort_rows, c->d_anchors, na, c->d_l1,
-                           c->d_meta, c->d_counters, s));
-        CU(cudaEventRecord(c->ev[1], s));
-        CU(launch_taskscan(c->d_meta, na, c->t, c->d_task_base, s));
-        const uint32_t* task_order = nullptr;
-        if (c->d_order && na > 0) {
-            uint32_t* k0 = c->d_order;
-            const long long oc = c->order_cap;
-            CU(launch_taskorder(c->W, c->d_table, c->d_l1, c->d_meta, c->d_anchors, c->d_task_base, na, c->K, oc, k0,
-                                k0 + 2 * oc, s));
-            size_t tb = c->order_tmp_bytes;
-            CU(cub::DeviceRadixSort::SortPairs(c->d_order_tmp, tb, k0, k0 + oc, k0 + 2 * oc, k0 + 3 * oc,
-                                               static_cast<int>(oc), 0, 8, s));
-            task_order = k0 + 3 * oc;
-        }
-        SearchParams P{};
-        P.n = c->n;
-        P.m = c->m;
-        P.l = c->l;
-        P.d = c->d;
-        P.w = c->w;
-        P.K = c->K;
-        P.t = c->t;
-        P.prune = c->opt.prune_level;
-        P.sort_rows = c->opt.sort_rows;
-        P.table = c->d_table;
-        P.l1_entries = c->d_l1;
-        P.l1_meta = c->d_meta;
-        P.anchor_off = c->d_anchors;
-        P.task_base = c->d_task_base;
-        P.task_order = task_order;
-        P.nanchors = na;
-        P.task_ai = c->d_task_ai;
-        P.task_u = c->d_task_u;
-        P.nexplicit = static_cast<long long>(c->task_u.size());
-        P.qs = c->d_qs;
-        P.qslots = c->d_qslots;
-        P.qstate = c->d_qstate;
-        P.qcap = c->qcap;
-        P.qslot_bytes = c->qslot_bytes;
-        P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
-        P.don_pushes = 32;  // DFS pushes between starvation checks (4: +1.8 % on (17,6), +1.6 % (21,8))
-        P.don_rounds_mask = 63;
-        P.don_burst = 1;
-        if (const char* e = std::getenv("PMS8G_DON_BURST")) P.don_burst = std::max(1, std::atoi(e));
-        if (const char* e = std::getenv("PMS8G_DON_PUSHES")) P.don_pushes = std::max(1, std::atoi(e));
-        if (const char* e = std::getenv("PMS8G_LOG_CYCLES")) P.log_cycles = std::atoll(e);
-        if (const char* e = std::getenv("PMS8G_DON_ROUNDS")) P.don_rounds_mask = std::max(1, std::atoi(e)) - 1;
-        P.lazy = (c->opt.exact_tree || std::getenv("PMS8G_EAGER")) ? 0 : 1;
-        P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
-        // the consensus row rule changes the tree (not the motif set): off for exact_tree
-        P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
-        if (P.cons_rows && std::getenv("PMS8G_CONS3")) P.cons_rows |= 2;  // also the t = 3 lazy rows (experiment)
-        P.plan = c->plan;
-        P.scratch = c->d_scratch;
-        P.scratch_words = c->scratch_words;
-        P.level_cap = c->level_cap;
-        P.node_cap = c->node_cap;
-        P.keys = c->d_keys;
-        P.key_count = c->d_key_count;
-        P.key_cap = c->key_cap;
-        P.counters = c->d_counters;
-        P.error_flag = c->d_err;
-        // cross-GPU claims: 4 tasks per NVLink CAS until the last 16 per warp of this device
-        P.claim_chunk = 4;
-        if (const char* e = std::getenv("PMS8G_CLAIM_CHUNK")) P.claim_chunk = std::max(1, std::atoi(e));
-        P.chunk_until = 16ll * c->blocks * c->warps;
-        P.jitter_ns = 1000ull * c->opt.jitter_max_us;
-        P.jitter_seed = c->opt.jitter_seed;
-        P.gqueue = nullptr;
-        P.gepoch = 0;
-        if (c->opt.queue && attempt == 0) {
-            P.gqueue = static_cast<unsigned long long*>(c->opt.queue->dptr);
-            P.gepoch = ++c->opt.queue->epoch;
-        }
-        // a retry (key buffer grown) searches every task locally: the shared
-        // counter's epoch stays in step with the other ranks, and this rank's
-        // result is a superset of its share (the union is unchanged)
         const char* tl_path = std::getenv("PMS8G_TIMELINE");  // diagnostics: task timeline dump
         unsigned long long* d_tl = nullptr;
-        if (tl_path) {
-            P.timeline_cap = 1 << 21;
-            CU(cudaMalloc(&d_tl, sizeof(unsigned long long) * 2 * P.timeline_cap));
-            P.timeline = d_tl;
+        if (c->sig) {
+            // alphabets of 5..32 symbols: B-plane l-mers (pms8g_sigma.cu)
+            CU(cudaMemsetAsync(c->d_task_counter, 0, sizeof(unsigned long long), s));
+            CU(launch_encode_sigma(c->B, c->d_codes, c->n, c->m, c->l, c->w, c->sigma, c->d_table, c->d_err, s));
+            CU(cudaEventRecord(c->ev[0], s));
+            CU(launch_rowbuild_sigma(c->B, c->d_table, c->n, c->w, c->d, c->K, c->d_anchors, na, c->d_l1, c->d_meta,
+                                     c->d_counters, s));
+            CU(cudaEventRecord(c->ev[1], s));
+            CU(launch_taskscan(c->d_meta, na, c->t, c->d_task_base, s));
+            SigmaParams SP{};
+            SP.n = c->n;
+            SP.m = c->m;
+            SP.l = c->l;
+            SP.d = c->d;
+            SP.w = c->w;
+            SP.K = c->K;
+            SP.t = c->t;
+            SP.sigma = c->sigma;
+            SP.prune = c->opt.prune_level;
+            SP.table = c->d_table;
+            SP.l1_entries = c->d_l1;
+            SP.l1_meta = c->d_meta;
+            SP.anchor_off = c->d_anchors;
+            SP.task_base = c->d_task_base;
+            SP.nanchors = na;
+            SP.next_task = c->d_task_counter;
+            SP.scratch = c->d_scratch;
+            SP.scratch_words = c->scratch_words;
+            SP.level_cap = c->level_cap;
+            SP.node_cap = c->node_cap;
+            SP.keys = c->d_keys;
+            SP.key_count = c->d_key_count;
+            SP.key_cap = c->key_cap;
+            SP.counters = c->d_counters;
+            SP.error_flag = c->d_err;
+            CU(cudaEventRecord(c->ev[2], s));
+            if (na > 0) CU(launch_search_sigma(c->B, SP, c->blocks, c->warps, s));
+            CU(cudaEventRecord(c->ev[3], s));
+        } else {
+            CU(launch_encode(c->W, c->d_codes, c->n, c->m, c->l, c->w, c->d_table, c->d_err, s));
+            CU(cudaEventRecord(c->ev[0], s));
+            CU(launch_rowbuild(c->W, c->d_table, c->n, c->w, c->d, c->K, c->opt.sort_rows, c->d_anchors, na, c->d_l1,
+                               c->d_meta, c->d_counters, s));
+            CU(cudaEventRecord(c->ev[1], s));
+            CU(launch_taskscan(c->d_meta, na, c->t, c->d_task_base, s));
+            const uint32_t* task_order = nullptr;
+            if (c->d_order && na > 0) {
+                uint32_t* k0 = c->d_order;
+                const long long oc = c->order_cap;
+                CU(launch_taskorder(c->W, c->d_table, c->d_l1, c->d_meta, c->d_anchors, c->d_task_base, na, c->K, oc, k0,
+                                    k0 + 2 * oc, s));
+                size_t tb = c->order_tmp_bytes;
+                CU(cub::DeviceRadixSort::SortPairs(c->d_order_tmp, tb, k0, k0 + oc, k0 + 2 * oc, k0 + 3 * oc,
+                                                   static_cast<int>(oc), 0, 8, s));
+                task_order = k0 + 3 * oc;
+            }
+            SearchParams P{};
+            P.n = c->n;
+            P.m = c->m;
+            P.l = c->l;
+            P.d = c->d;
+            P.w = c->w;
+            P.K = c->K;
+            P.t = c->t;
+            P.prune = c->opt.prune_level;
+            P.sort_rows = c->opt.sort_rows;
+            P.table = c->d_table;
+            P.l1_entries = c->d_l1;
+            P.l1_meta = c->d_meta;
+            P.anchor_off = c->d_anchors;
+            P.task_base = c->d_task_base;
+            P.task_order = task_order;
+            P.nanchors = na;
+            P.task_ai = c->d_task_ai;
+            P.task_u = c->d_task_u;
+            P.nexplicit = static_cast<long long>(c->task_u.size());
+            P.qs = c->d_qs;
+            P.qslots = c->d_qslots;
+            P.qstate = c->d_qstate;
+            P.qcap = c->qcap;
+            P.qslot_bytes = c->qslot_bytes;
+            P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
+            P.don_pushes = 32;  // DFS pushes between starvation checks (4: +1.8 % on (17,6), +1.6 % (21,8))
+            P.don_rounds_mask = 63;
+            P.don_burst = 1;
+            if (const char* e = std::getenv("PMS8G_DON_BURST")) P.don_burst = std::max(1, std::atoi(e));
+            if (const char* e = std::getenv("PMS8G_DON_PUSHES")) P.don_pushes = std::max(1, std::atoi(e));
+            if (const char* e = std::getenv("PMS8G_LOG_CYCLES")) P.log_cycles = std::atoll(e);
+            if (const char* e = std::getenv("PMS8G_DON_ROUNDS")) P.don_rounds_mask = std::max(1, std::atoi(e)) - 1;
+            P.lazy = (c->opt.exact_tree || std::getenv("PMS8G_EAGER")) ? 0 : 1;
+            P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
+            // the consensus row rule changes the tree (not the motif set): off for exact_tree
+            P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
+            if (P.cons_rows && std::getenv("PMS8G_CONS3")) P.cons_rows |= 2;  // also the t = 3 lazy rows (experiment)
+            P.plan = c->plan;
+            P.scratch = c->d_scratch;
+            P.scratch_words = c->scratch_words;
+            P.level_cap = c->level_cap;
+            P.node_cap = c->node_cap;
+            P.keys = c->d_keys;
+            P.key_count = c->d_key_count;
+            P.key_cap = c->key_cap;
+            P.counters = c->d_counters;
+            P.error_flag = c->d_err;
+            // cross-GPU claims: 4 tasks per NVLink CAS until the last 16 per warp of this device
+            P.claim_chunk = 4;
+            if (const char* e = std::getenv("PMS8G_CLAIM_CHUNK")) P.claim_chunk = std::max(1, std::atoi(e));
+            P.chunk_until = 16ll * c->blocks * c->warps;
+            P.jitter_ns = 1000ull * c->opt.jitter_max_us;
+            P.jitter_seed = c->opt.jitter_seed;
+            P.gqueue = nullptr;
+            P.gepoch = 0;
+            if (c->opt.queue && attempt == 0) {
+                P.gqueue = static_cast<unsigned long long*>(c->opt.queue->dptr);
+                P.gepoch = ++c->opt.queue->epoch;
+            }
+            // a retry (key buffer grown) searches every task locally: the shared
+            // counter's epoch stays in step with the other ranks, and this rank's
+            // result is a superset of its share (the union is unchanged)
+            if (tl_path) {
+                P.timeline_cap = 1 << 21;
+                CU(cudaMalloc(&d_tl, sizeof(unsigned long long) * 2 * P.timeline_cap));
+                P.timeline = d_tl;
+            }
+            CU(cudaEventRecord(c->ev[2], s));
+            // the dynamic shared-memory limit is a per-kernel attribute, shared by
+            // every context of this (W, t) build in the process: set it per launch
+            if (na > 0) {
+                CU(set_search_smem(c->W, c->t, c->smem));
+                CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
+            }
+            CU(cudaEventRecord(c->ev[3], s));
         }
-        CU(cudaEventRecord(c->ev[2], s));
-        // the dynamic shared-memory limit is a per-kernel attribute, shared by
-        // every context of this (W, t) build in the process: set it per launch
-        if (na > 0) {
-            CU(set_search_smem(c->W, c->t, c->smem));
-            CU(launch_search(c->W, P, c->blocks, c->warps, c->smem, s));
-        }
-        CU(cudaEventRecord(c->ev[3], s));
         CU(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long) * C_NCTR, cudaMemcpyDeviceToHost,
                            s));
         CU(cudaMemcpyAsync(c->h_counters + C_NCTR, c->d_key_count, sizeof(unsigned long long),
@@ -1204,7 +1281,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
         CU(cudaStreamSynchronize(s));
         CU(cudaGetLastError());
         if (d_tl) {
-            const long long ntl = std::min<long long>(static_cast<long long>(c->h_counters[C_TLN]), P.timeline_cap);
+            const long long ntl = std::min<long long>(static_cast<long long>(c->h_counters[C_TLN]), 1ll << 21);
             std::vector<unsigned long long> h(2 * static_cast<size_t>(ntl));
             CU(cudaMemcpy(h.data(), d_tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
             CU(cudaFree(d_tl));
@@ -1213,7 +1290,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
                 std::fclose(f);
             }
         }
-        if (c->h_err[0] & 1) return fail(err, errlen, PMS8G_ERR_INVALID, "symbol code outside the 2-bit alphabet");
+        if (c->h_err[0] & 1) return fail(err, errlen, PMS8G_ERR_INVALID, "symbol code outside the alphabet");
         // worker failures name the subproblem like run_parallel (src/parallel.cpp:66-86)
         char where[64] = "search";
         if (c->h_err[1] > 0) std::snprintf(where, sizeof where, "subproblem at offset %d", c->h_err[1] - 1);
@@ -1241,7 +1318,7 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             size_t bytes = c->cub_bytes;
             CU(cub::DeviceRadixSort::SortKeys(c->d_cub, bytes, reinterpret_cast<K128*>(c->d_keys),
                                               reinterpret_cast<K128*>(c->d_keys_sorted), static_cast<int>(raw), 0,
-                                              2 * c->l, s));
+                                              c->key_bits(), s));
             bytes = c->cub_bytes;
             CU(cub::DeviceSelect::Unique(c->d_cub, bytes, reinterpret_cast<K128*>(c->d_keys_sorted),
                                          reinterpret_cast<K128*>(c->d_keys_unique), c->d_unique_count,
@@ -1251,7 +1328,12 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             if (c->opt.reverify) {
                 CU(cudaStreamSynchronize(s));
                 uniq = static_cast<long long>(c->h_counters[C_NCTR + 1]);
-                CU(launch_reverify(c->W, c->d_table, c->n, c->w, c->l, c->d, c->d_keys_unique, uniq, c->d_fail, s));
+                if (c->sig)
+                    CU(launch_reverify_sigma(c->B, c->d_table, c->n, c->w, c->l, c->d, c->d_keys_unique, uniq,
+                                             c->d_fail, s));
+                else
+                    CU(launch_reverify(c->W, c->d_table, c->n, c->w, c->l, c->d, c->d_keys_unique, uniq, c->d_fail,
+                                       s));
                 CU(cudaMemcpyAsync(c->h_err + 2, c->d_fail, sizeof(int), cudaMemcpyDeviceToHost, s));
             }
             CU(cudaStreamSynchronize(s));
@@ -1302,7 +1384,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
                       sizeof(uint32_t) * 4 * static_cast<size_t>(c->order_cap) +
                       static_cast<size_t>(c->qcap) * (c->qslot_bytes + sizeof(unsigned int)) +
                       (c->scratch_words * 4 * nwarps - lvl));
-            R.packed_words = words(static_cast<size_t>(c->n) * c->m + static_cast<size_t>(c->K) * lmer_bytes(c->W));
+            R.packed_words = words(static_cast<size_t>(c->n) * c->m +
+                                   static_cast<size_t>(c->K) * (c->sig ? sigma_lmer_bytes(c->B) : lmer_bytes(c->W)));
             R.lookup_table_words = 0;
         }
         R.wall_seconds = now_s() - t0;

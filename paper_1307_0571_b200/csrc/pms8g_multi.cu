@@ -162,6 +162,9 @@ int pms8g_multi_create(int n, int m, int l, int d, const char* alphabet, const p
         if (!can) reach = false;
     }
     if (std::getenv("PMS8G_MULTI_STATIC")) reach = false;
+    // alphabets of 5+ symbols run the B-plane search, which claims from its
+    // device-local counter: split the S1 offsets statically
+    if (alphabet && std::strlen(alphabet) > 4) reach = false;
     int rc = PMS8G_OK;
     auto bail = [&](int code) {
         destroy_multi(h);

@@ -8,6 +8,7 @@ build container (it needs /root/reference to build oracle/_ref); the fixtures
 it writes are committed and travel to the GPU box.
 
     python tests/golden/make_golden.py quick        # seconds-to-minutes parts
+    python tests/golden/make_golden.py protein      # alphabets of 5..32 symbols (seconds)
     python tests/golden/make_golden.py heavy17      # (17,6) seeds 1-5 full runs
     python tests/golden/make_golden.py heavy21      # (21,8) anchor sample
     python tests/golden/make_golden.py heavy21full  # (21,8) every S1 l-mer (~1.5 h on 8 threads)
@@ -121,6 +122,45 @@ def small_random():
     dump("small_random.json", out)
 
 
+def protein():
+    """Alphabets of 5..32 symbols (the B-plane GPU path): planted protein
+    instances from the reference generator and small random instances over
+    custom alphabets, motif sets from the reference's run_parallel."""
+    def solve_alpha(seqs, l, d, t, alphabet):
+        with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+            f.write("\n".join(seqs) + "\n")
+            path = f.name
+        try:
+            return parse_solve(run("file", path, l, d, 1, t, alphabet))
+        finally:
+            os.unlink(path)
+
+    out = []
+    for (l, d, n, m, seed, t) in [(8, 1, 10, 60, 1, 0), (10, 2, 10, 60, 2, 0), (12, 3, 8, 50, 3, 0),
+                                  (13, 4, 6, 40, 4, 0), (9, 2, 12, 80, 5, 0), (10, 2, 10, 60, 2, 3),
+                                  (12, 3, 8, 50, 3, 4), (11, 3, 6, 30, 6, 0)]:
+        lines = run("gen", l, d, seed, n, m, "exact", "protein").strip().split("\n")
+        motif, seqs = lines[0].split()[1], lines[2:]
+        motifs, rep = solve_alpha(seqs, l, d, t, "protein")
+        out.append({"alphabet": "protein", "l": l, "d": d, "t": t, "seed": seed, "planted": motif,
+                    "sequences": seqs, "motifs": motifs, "threshold": rep["threshold"]})
+    rng = np.random.default_rng(20261021)
+    alphas = ["custom:ACGTN", "custom:ABCDEFGH", "protein", "custom:ABCDEFGHIJKLMNOPQRSTUVWXYZ012345",
+              "custom:ZYXWVUTSRQ"]
+    for i in range(60):
+        a = alphas[i % len(alphas)]
+        sym = "ACDEFGHIKLMNPQRSTVWY" if a == "protein" else a.split(":", 1)[1]
+        n = int(rng.integers(2, 6))
+        l = int(rng.integers(3, 8))
+        m = int(rng.integers(l, 26))
+        d = int(rng.integers(0, 3))
+        seqs = ["".join(sym[x] for x in rng.integers(0, len(sym), m)) for _ in range(n)]
+        motifs, rep = solve_alpha(seqs, l, d, 0, a)
+        out.append({"alphabet": a, "l": l, "d": d, "t": 0, "seed": None, "planted": None, "sequences": seqs,
+                    "motifs": motifs, "threshold": rep["threshold"]})
+    dump("protein.json", out)
+
+
 def planted_full(l, d, seeds, name):
     out = []
     for seed in seeds:
@@ -166,6 +206,8 @@ def main():
         instances()
         small_random()
         planted_full(13, 4, [1, 2, 3, 4, 5], "planted_13_4.json")
+    elif what == "protein":
+        protein()
     elif what == "heavy17":
         planted_full(17, 6, [1, 2, 3, 4, 5], "planted_17_6.json")
     elif what == "heavy21":

@@ -94,3 +94,17 @@ def test_threshold_invariance_on_small_instance():
     for t in (1, 3, 4, 6):
         assert O.solve(codes, 9, 2, t=t)[0] == base
     assert base == O.brute_force(codes, 9, 2)
+
+
+def _protein_symbols(name):
+    return "ACDEFGHIKLMNPQRSTVWY" if name == "protein" else name.split(":", 1)[1]
+
+
+def test_oracle_matches_reference_on_larger_alphabets():
+    # tests/golden/protein.json: the reference's run_parallel over alphabets of
+    # 5..32 symbols (make_golden.py protein); the C restatement must agree
+    for case in golden("protein.json"):
+        sym = _protein_symbols(case["alphabet"])
+        codes = O.codes_of(case["sequences"], sym)
+        got, _ = O.solve(codes, case["l"], case["d"], case["t"], sigma=len(sym), alphabet=sym, cap=1 << 14)
+        assert sorted(got) == case["motifs"], case["alphabet"]
