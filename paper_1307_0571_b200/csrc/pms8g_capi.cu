@@ -59,6 +59,7 @@ unsigned __int128 nsize(int l, int d, int sigma) {
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
     int ref_t = 0;  // the reference's switch depth (override or estimate_threshold), reported
+    bool table_global = false;  // l-mer table read from global memory (too large for shared memory)
     int B = 2;          // bits (planes) per symbol: 2 for sigma <= 4 (two-plane DNA path), else ceil(log2 sigma)
     bool sig = false;   // sigma > 4: the B-plane search (pms8g_sigma.cu)
     int key_bits() const { return B * l; }
@@ -549,13 +550,18 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     } else {
         c->plan = make_plan(c->W, l, t);
         int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
+        const int want = warps;
         while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap) --warps;  // + static smem
-        if (search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap)
-            return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID,
-                                     "l-mer table of %d l-mers does not fit shared memory (%zu bytes)", c->K,
-                                     smem_cap));
+        // a table that leaves fewer than half the warps (or none) stays in
+        // global memory instead: L2-resident, read through L1
+        c->table_global = std::getenv("PMS8G_GLOBAL_TABLE") != nullptr || 2 * warps < want ||
+                          search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap;
+        if (c->table_global) {
+            warps = want;
+            while (warps > 1 && search_smem(c->W, 0, warps, c->plan) + 64 > smem_cap) --warps;
+        }
         c->warps = warps;
-        c->smem = search_smem(c->W, c->K, warps, c->plan);
+        c->smem = search_smem(c->W, c->table_global ? 0 : c->K, warps, c->plan);
         c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
         // clusters of search_cluster(W) CTAs share the l-mer table: whole clusters only
         const int cs = search_cluster(c->W);
@@ -1233,8 +1239,8 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             P.reorder = (c->opt.exact_tree || std::getenv("PMS8G_NATURAL_ORDER")) ? 0 : 1;
             // the consensus row rule changes the tree (not the motif set): off for exact_tree
             P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
-            if (P.cons_rows && std::getenv("PMS8G_CONS3")) P.cons_rows |= 2;  // also the t = 3 lazy rows (experiment)
-            P.plan = c->plan;
+                P.plan = c->plan;
+            P.table_global = c->table_global ? 1 : 0;
             P.scratch = c->d_scratch;
             P.scratch_words = c->scratch_words;
             P.level_cap = c->level_cap;

@@ -82,6 +82,29 @@ struct WarpFixed {
 
 constexpr int MAXCH = 5;  // candidate chunks of 32 held in registers by verify
 
+// Read-only table load through the non-coherent L1 path (global tables).
+template <int W>
+__device__ __forceinline__ Lmer<W> ldg_lmer(const Lmer<W>* p) {
+    Lmer<W> x;
+    if constexpr (W == 2) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+        x.h[0] = v.x;
+        x.h[W - 1] = v.y;
+        x.o[0] = v.z;
+        x.o[W - 1] = v.w;
+    } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        x.h[0] = v.x;
+        x.o[0] = v.y;
+    }
+    return x;
+}
+
+template <int W>
+__device__ __forceinline__ const Lmer<W>* global_table(uint32_t lo, uint32_t hi) {
+    return reinterpret_cast<const Lmer<W>*>((static_cast<unsigned long long>(hi) << 32) | lo);
+}
+
 // Two-word l-mers (16 B each) would take 176 KB of a 227 KB CTA for n=20,
 // m=600, leaving room for 7 warps; split over a 2-CTA cluster each SM holds
 // 88 KB and runs 16 warps.
@@ -103,6 +126,8 @@ struct WarpCtx {
     // (ids < thalf in rank 0's shared memory, the rest in rank 1's), read
     // through distributed shared memory; tb[r] = shared::cluster address of
     // rank r's half
+    // Tables too large for shared memory stay in global memory (L2-resident,
+    // read through L1): then thalf == 0 and tb holds the 64-bit table address.
     uint32_t tb[2];
     uint32_t thalf;
     // shared-memory views derived from the extern __shared__ symbol, so every
@@ -111,6 +136,7 @@ struct WarpCtx {
     // l-mer `id` of the table (one-word: local LDS.64; two-word: one
     // LD.shared::cluster.v4 from whichever CTA of the pair holds it)
     __device__ __forceinline__ Lmer<W> lmer(uint32_t id) const {
+        if (thalf == 0u) return ldg_lmer<W>(global_table<W>(tb[0], tb[1]) + id);
         if constexpr (kClusterTable<W>) {
             const uint32_t r = id >= thalf ? 1u : 0u;
             const uint32_t addr = tb[r] + (id - r * thalf) * static_cast<uint32_t>(sizeof(Lmer<W>));
@@ -141,8 +167,9 @@ struct WarpCtx {
 // itself lives in local memory across the noinline calls).
 template <int W>
 struct TableRef {
-    uint32_t tb0, tb1, thalf;
+    uint32_t tb0, tb1, thalf;  // as WarpCtx: thalf == 0 -> global table at (tb1 << 32 | tb0)
     __device__ __forceinline__ Lmer<W> get(uint32_t id) const {
+        if (thalf == 0u) return ldg_lmer<W>(global_table<W>(tb0, tb1) + id);
         if constexpr (kClusterTable<W>) {
             const bool hi = id >= thalf;
             const uint32_t addr = (hi ? tb1 : tb0) + (hi ? id - thalf : id) * static_cast<uint32_t>(sizeof(Lmer<W>));
@@ -381,7 +408,7 @@ __device__ __forceinline__ bool cons_pass(const ConsMasks<W>& cm, const Lmer<W>&
 // members (k >= 2), full pruning, t >= 4 builds.
 template <int MT>
 __device__ __forceinline__ bool cons_rows_at(const SearchParams& P, int k) {
-    return (MT >= 4 || (MT == 3 && (P.cons_rows & 2))) && (P.cons_rows & 1) && k >= 2;
+    return MT >= 4 && P.cons_rows && k >= 2;
 }
 
 // One claim attempt by lane 0: 0 static task, 1 dynamic task (idx set),
@@ -572,17 +599,27 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     };
     // software pipeline: entries two blocks ahead, their l-mers (table reads,
     // DSMEM for two-word l-mers) one block ahead
+    // (t >= 4 builds; the t <= 3 builds keep the one-block entry prefetch:
+    // their register budget goes to the enumeration and verification loops)
+    constexpr bool kPipeV = MT >= 4;
     uint32_t e_next = load_entry(lane);
-    uint32_t e_next2 = load_entry(lane + 32);
-    Lmer<W> V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
+    uint32_t e_next2 = kPipeV ? load_entry(lane + 32) : 0u;
+    Lmer<W> V_next;
+    if constexpr (kPipeV) V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
     for (int base = 0; base < n_iter; base += 32) {
         const int f = base + lane;
         const bool valid = f < n_iter;
         const uint32_t e = e_next;
-        const Lmer<W> V = V_next;
-        e_next = e_next2;
-        e_next2 = load_entry(f + 64);
-        if (base + 32 < n_iter) V_next = tr.get(f + 32 < n_iter ? e_next & ID_MASK : 0u);
+        Lmer<W> V;
+        if constexpr (kPipeV) {
+            V = V_next;
+            e_next = e_next2;
+            e_next2 = load_entry(f + 64);
+            if (base + 32 < n_iter) V_next = tr.get(f + 32 < n_iter ? e_next & ID_MASK : 0u);
+        } else {
+            e_next = load_entry(f + 32);
+            if (valid) V = tr.get(e & ID_MASK);
+        }
         bool keep = false;
         if (valid) {
             // the consensus rule first: at deep levels it rejects most slots
@@ -701,17 +738,25 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     ss.load(C, k, U);
     int out = 0;
     // entries two blocks ahead, their l-mers one block ahead (as filter_push)
+    constexpr bool kPipeV = MT >= 4;
     uint32_t e_next = lane < cnt ? src[lane] : 0u;
-    uint32_t e_next2 = lane + 32 < cnt ? src[lane + 32] : 0u;
-    Lmer<W> V_next = tr.get(e_next & ID_MASK);
+    uint32_t e_next2 = kPipeV && lane + 32 < cnt ? src[lane + 32] : 0u;
+    Lmer<W> V_next;
+    if constexpr (kPipeV) V_next = tr.get(e_next & ID_MASK);
     for (int base = 0; base < cnt; base += 32) {
         const int f = base + lane;
         bool keep = false;
         const uint32_t e = e_next;
-        const Lmer<W> V = V_next;
-        e_next = e_next2;
-        e_next2 = f + 64 < cnt ? src[f + 64] : 0u;
-        if (base + 32 < cnt) V_next = tr.get(e_next & ID_MASK);
+        Lmer<W> V;
+        if constexpr (kPipeV) {
+            V = V_next;
+            e_next = e_next2;
+            e_next2 = f + 64 < cnt ? src[f + 64] : 0u;
+            if (base + 32 < cnt) V_next = tr.get(e_next & ID_MASK);
+        } else {
+            e_next = f + 32 < cnt ? src[f + 32] : 0u;
+            if (f < cnt) V = tr.get(e & ID_MASK);
+        }
         if (f < cnt) {
             keep = !cons || cons_pass<W>(cm, V);
             Mask<W> mu;
@@ -2042,7 +2087,19 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     const Lmer<W>* gT = static_cast<const Lmer<W>*>(P.table);
     WarpCtx<W, MT> C;
     uint32_t table_rows = static_cast<uint32_t>(P.K);
-    if constexpr (kClusterTable<W>) {
+    if (P.table_global) {
+        // the table stays in global memory; nothing to stage
+        const unsigned long long ga = reinterpret_cast<unsigned long long>(gT);
+        C.tb[0] = static_cast<uint32_t>(ga);
+        C.tb[1] = static_cast<uint32_t>(ga >> 32);
+        C.thalf = 0u;
+        table_rows = 0;
+        if constexpr (kClusterTable<W>) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    } else if constexpr (kClusterTable<W>) {
         // this CTA's half of the table; the pair's halves are read through DSMEM
         uint32_t rank;
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -2285,6 +2342,7 @@ size_t node_bytes(int W) { return W == 1 ? sizeof(Node<1>) : sizeof(Node<2>); }
 int search_cluster(int W) { return W == 2 ? 2 : 1; }
 
 size_t search_smem(int W, int K, int warps, const WarpPlan& plan) {
+    // K == 0: the table stays in global memory
     const size_t rows = (static_cast<size_t>(K) + search_cluster(W) - 1) / search_cluster(W);
     return (rows * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
 }

@@ -78,12 +78,12 @@ def instances():
     dump("instances.json", out)
 
 
-def solve_file(seqs, l, d, t=0):
+def solve_file(seqs, l, d, t=0, threads=1):
     with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
         f.write("\n".join(seqs) + "\n")
         path = f.name
     try:
-        return parse_solve(run("file", path, l, d, 1, t))
+        return parse_solve(run("file", path, l, d, threads, t))
     finally:
         os.unlink(path)
 
@@ -208,6 +208,18 @@ def main():
         planted_full(13, 4, [1, 2, 3, 4, 5], "planted_13_4.json")
     elif what == "protein":
         protein()
+    elif what == "large":
+        # beyond the shared-memory table: n=20, m=2000, l=50 (K = 39,020 two-word
+        # l-mers, 624 KB), the reference's run_parallel on the whole instance
+        out = []
+        for (l, d, seed, n, m) in [(50, 12, 7, 20, 2000), (40, 10, 8, 20, 2000)]:
+            motif, pos, seqs = gen(l, d, seed, n, m)
+            motifs, rep = solve_file(seqs, l, d, 0, threads=int(os.environ.get("GOLDEN_THREADS", THREADS)))
+            out.append({"l": l, "d": d, "seed": seed, "n": n, "m": m, "motif": motif, "motifs": motifs,
+                        "threshold": rep["threshold"], "wall_seconds": rep["wall_seconds"],
+                        "sha256": hashlib.sha256("\n".join(seqs).encode()).hexdigest()})
+            print(l, d, len(motifs), rep["wall_seconds"])
+        dump("large.json", out)
     elif what == "heavy17":
         planted_full(17, 6, [1, 2, 3, 4, 5], "planted_17_6.json")
     elif what == "heavy21":

@@ -100,7 +100,7 @@ def test_deep_switch_depths_against_oracle(l, d, n, m, seed):
     inst = planted(l, d, seed, n=n, m=m)
     want, _ = O.solve(inst.codes, l, d)
     assert inst.motif in want
-    for t in range(2, min(n, 6) + 1):
+    for t in range(3 if l > 32 else 2, min(n, 6) + 1):  # t=2 on l > 32: minutes of enumeration
         assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == want, t
 
 
@@ -360,3 +360,29 @@ def test_worker_failure_names_the_subproblem(monkeypatch):
     inst = planted(17, 6, 1)
     with pytest.raises(P.SolverRuntimeError, match=r"^subproblem at offset \d+ failed: enumeration stack overflow"):
         P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=list(range(0, 584, 8))))
+
+
+def test_global_table_mode_matches(monkeypatch):
+    # the l-mer table read from global memory (the mode instances beyond
+    # shared memory use) gives the same motif sets; anchor lists bypass the
+    # library's context cache, so the mode is chosen afresh
+    monkeypatch.setenv("PMS8G_GLOBAL_TABLE", "1")
+    g = golden("planted_17_6.json")[0]
+    inst = planted(17, 6, 1)
+    assert P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=list(range(584)))) == g["motifs"]
+    g = golden("planted_13_4.json")[1]
+    inst = planted(13, 4, 2)
+    assert P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(anchors=list(range(588)))) == g["motifs"]
+    _branch_parity("branches_50_21.json")
+
+
+def test_large_instances_beyond_shared_memory():
+    # n=20, m=2000: 39,020 two-word l-mers (624 KB) cannot be staged in shared
+    # memory; the reference's motif sets (tests/golden/large.json)
+    path = os.path.join(ROOT, "tests", "golden", "large.json")
+    if not os.path.exists(path):
+        pytest.skip("large.json not generated")
+    for case in golden("large.json"):
+        inst = planted(case["l"], case["d"], case["seed"], n=case["n"], m=case["m"])
+        assert case["motif"] == inst.motif
+        assert P.solve(inst.problem) == case["motifs"], (case["l"], case["d"])
