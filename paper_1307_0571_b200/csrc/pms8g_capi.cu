@@ -59,7 +59,6 @@ unsigned __int128 nsize(int l, int d, int sigma) {
 struct pms8g_ctx {
     int n = 0, m = 0, l = 0, d = 0, sigma = 0, W = 1, w = 0, K = 0, t = 0;
     int ref_t = 0;  // the reference's switch depth (override or estimate_threshold), reported
-    bool table_global = false;  // l-mer table read from global memory (too large for shared memory)
     int B = 2;          // bits (planes) per symbol: 2 for sigma <= 4 (two-plane DNA path), else ceil(log2 sigma)
     bool sig = false;   // sigma > 4: the B-plane search (pms8g_sigma.cu)
     int key_bits() const { return B * l; }
@@ -548,24 +547,27 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
         c->smem = sigma_warp_smem() * c->warps;
         c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
     } else {
-        c->plan = make_plan(c->W, l, t);
-        int warps = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, c->t);
-        const int want = warps;
-        while (warps > 1 && search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap) --warps;  // + static smem
-        // a table that leaves fewer than half the warps (or none) stays in
-        // global memory instead: L2-resident, read through L1
-        c->table_global = std::getenv("PMS8G_GLOBAL_TABLE") != nullptr || 2 * warps < want ||
-                          search_smem(c->W, c->K, warps, c->plan) + 64 > smem_cap;
-        if (c->table_global) {
-            warps = want;
-            while (warps > 1 && search_smem(c->W, 0, warps, c->plan) + 64 > smem_cap) --warps;
+        // one-word l-mers: table in shared memory; if it leaves fewer than
+        // half the warps, the instance runs the two-word build (table in
+        // global memory, upper words zero) — DESIGN.md §3
+        auto fit = [&](int W, int want) {
+            const WarpPlan plan = make_plan(W, l, t);
+            int wp = want;
+            while (wp > 1 && search_smem(W, c->K, wp, plan) + 64 > smem_cap) --wp;  // + static smem
+            return search_smem(W, c->K, wp, plan) + 64 > smem_cap ? 0 : wp;
+        };
+        if (c->W == 1) {
+            const int want = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(1, t);
+            if (std::getenv("PMS8G_GLOBAL_TABLE") || 2 * fit(1, want) < want) c->W = 2;
         }
-        c->warps = warps;
-        c->smem = search_smem(c->W, c->table_global ? 0 : c->K, warps, c->plan);
+        c->plan = make_plan(c->W, l, t);
+        const int want = opt.warps_per_block > 0 ? std::min(opt.warps_per_block, 16) : search_default_warps(c->W, t);
+        c->warps = fit(c->W, want);
+        if (c->warps == 0)
+            return cleanup_fail(fail(err, errlen, PMS8G_ERR_INVALID, "per-warp state of %d warps does not fit %zu bytes",
+                                     want, smem_cap));
+        c->smem = search_smem(c->W, c->K, c->warps, c->plan);
         c->blocks = opt.grid_blocks > 0 ? opt.grid_blocks : c->sms * (opt.blocks_per_sm > 0 ? opt.blocks_per_sm : 1);
-        // clusters of search_cluster(W) CTAs share the l-mer table: whole clusters only
-        const int cs = search_cluster(c->W);
-        c->blocks = std::max(cs, c->blocks / cs * cs);
         if (set_search_smem(c->W, c->t, c->smem) != cudaSuccess)
             return cleanup_fail(fail(err, errlen, PMS8G_ERR_CUDA, "cannot set shared memory size %zu", c->smem));
     }
@@ -1240,7 +1242,6 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             // the consensus row rule changes the tree (not the motif set): off for exact_tree
             P.cons_rows = (c->opt.prune_level == 2 && !c->opt.exact_tree && !std::getenv("PMS8G_NO_CONS_ROWS")) ? 1 : 0;
                 P.plan = c->plan;
-            P.table_global = c->table_global ? 1 : 0;
             P.scratch = c->d_scratch;
             P.scratch_words = c->scratch_words;
             P.level_cap = c->level_cap;

@@ -142,7 +142,6 @@ struct SearchParams {
     unsigned long long jitter_ns;
     unsigned long long jitter_seed;
     int cons_rows;  // 1: push filters apply the stack consensus bound to every remaining row
-    int table_global;               // 1: the l-mer table is read from global memory (too large for smem)
     int claim_chunk;                // shared queue: static tasks per CAS far from the tail
     long long chunk_until;          // ... while more than this many remain
 };

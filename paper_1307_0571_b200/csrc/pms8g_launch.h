@@ -13,7 +13,6 @@ size_t lmer_bytes(int W);
 size_t node_bytes(int W);
 WarpPlan make_plan(int W, int l, int t);
 size_t search_smem(int W, int K, int warps, const WarpPlan& plan);
-int search_cluster(int W);  // CTAs per cluster of the search kernel (the l-mer table is split over them)
 size_t task_slot_bytes(int W);
 
 cudaError_t launch_encode(int W, const uint8_t* codes, int n, int m, int l, int w, void* table, int* err,

@@ -100,16 +100,17 @@ __device__ __forceinline__ Lmer<W> ldg_lmer(const Lmer<W>* p) {
     return x;
 }
 
-template <int W>
-__device__ __forceinline__ const Lmer<W>* global_table(uint32_t lo, uint32_t hi) {
-    return reinterpret_cast<const Lmer<W>*>((static_cast<unsigned long long>(hi) << 32) | lo);
-}
 
-// Two-word l-mers (16 B each) would take 176 KB of a 227 KB CTA for n=20,
-// m=600, leaving room for 7 warps; split over a 2-CTA cluster each SM holds
-// 88 KB and runs 16 warps.
+// Where the l-mer table lives. One-word l-mers (8 B) are staged in every
+// CTA's shared memory (94 KB for n=20, m=600). Two-word l-mers (16 B: 176 KB
+// for (50,21)) would leave room for 7 warps per SM, so their table stays in
+// global memory, L2-resident and read through L1 with 16 warps per SM:
+// measured (50,21) 617 ms per 12-S1-l-mer sample, against 634 ms with the
+// table split over 2-CTA clusters and read through DSMEM, and 3.3x slower
+// with 7 warps. One-word instances whose table does not fit
+// shared memory run the two-word build (upper words zero).
 template <int W>
-constexpr bool kClusterTable = W == 2;
+constexpr bool kGlobalTable = W == 2;
 
 template <int W, int MT>
 struct WarpCtx {
@@ -122,37 +123,14 @@ struct WarpCtx {
     int lane;
     int pushes_since_check;
     unsigned int checks;  // starvation checks made (lane 0; heartbeat pacing)
-    // two-word l-mers: the table is split over the CTA pair of a cluster
-    // (ids < thalf in rank 0's shared memory, the rest in rank 1's), read
-    // through distributed shared memory; tb[r] = shared::cluster address of
-    // rank r's half
-    // Tables too large for shared memory stay in global memory (L2-resident,
-    // read through L1): then thalf == 0 and tb holds the 64-bit table address.
-    uint32_t tb[2];
-    uint32_t thalf;
+    const Lmer<W>* gt;  // two-word builds: the table in global memory
     // shared-memory views derived from the extern __shared__ symbol, so every
     // access compiles to LDS/STS rather than generic LD/ST
     __device__ __forceinline__ const Lmer<W>* T() const { return reinterpret_cast<const Lmer<W>*>(dyn_smem); }
-    // l-mer `id` of the table (one-word: local LDS.64; two-word: one
-    // LD.shared::cluster.v4 from whichever CTA of the pair holds it)
+    // l-mer `id` of the table (one-word: LDS.64; two-word: LDG.128 via L1)
     __device__ __forceinline__ Lmer<W> lmer(uint32_t id) const {
-        if (thalf == 0u) return ldg_lmer<W>(global_table<W>(tb[0], tb[1]) + id);
-        if constexpr (kClusterTable<W>) {
-            const uint32_t r = id >= thalf ? 1u : 0u;
-            const uint32_t addr = tb[r] + (id - r * thalf) * static_cast<uint32_t>(sizeof(Lmer<W>));
-            uint32_t a, b, c, e;
-            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
-                         : "r"(addr));
-            Lmer<W> x;
-            x.h[0] = a;
-            x.h[W - 1] = b;
-            x.o[0] = c;
-            x.o[W - 1] = e;
-            return x;
-        } else {
-            return T()[id];
-        }
+        if constexpr (kGlobalTable<W>) return ldg_lmer<W>(gt + id);
+        else return T()[id];
     }
     __device__ __forceinline__ WarpFixed* S() const { return reinterpret_cast<WarpFixed*>(dyn_smem + off_S); }
     __device__ __forceinline__ uint8_t* thr() const { return dyn_smem + off_thr; }
@@ -167,34 +145,17 @@ struct WarpCtx {
 // itself lives in local memory across the noinline calls).
 template <int W>
 struct TableRef {
-    uint32_t tb0, tb1, thalf;  // as WarpCtx: thalf == 0 -> global table at (tb1 << 32 | tb0)
+    const Lmer<W>* gt;  // two-word builds
     __device__ __forceinline__ Lmer<W> get(uint32_t id) const {
-        if (thalf == 0u) return ldg_lmer<W>(global_table<W>(tb0, tb1) + id);
-        if constexpr (kClusterTable<W>) {
-            const bool hi = id >= thalf;
-            const uint32_t addr = (hi ? tb1 : tb0) + (hi ? id - thalf : id) * static_cast<uint32_t>(sizeof(Lmer<W>));
-            uint32_t a, b, c, e;
-            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
-                         : "r"(addr));
-            Lmer<W> x;
-            x.h[0] = a;
-            x.h[W - 1] = b;
-            x.o[0] = c;
-            x.o[W - 1] = e;
-            return x;
-        } else {
-            return reinterpret_cast<const Lmer<W>*>(dyn_smem)[id];
-        }
+        if constexpr (kGlobalTable<W>) return ldg_lmer<W>(gt + id);
+        else return reinterpret_cast<const Lmer<W>*>(dyn_smem)[id];
     }
 };
 
 template <int W, int MT>
 __device__ __forceinline__ TableRef<W> table_ref(const WarpCtx<W, MT>& C) {
     TableRef<W> t;
-    t.tb0 = C.tb[0];
-    t.tb1 = C.tb[1];
-    t.thalf = C.thalf;
+    t.gt = C.gt;
     return t;
 }
 
@@ -2086,38 +2047,13 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     Lmer<W>* T = reinterpret_cast<Lmer<W>*>(dyn_smem);
     const Lmer<W>* gT = static_cast<const Lmer<W>*>(P.table);
     WarpCtx<W, MT> C;
-    uint32_t table_rows = static_cast<uint32_t>(P.K);
-    if (P.table_global) {
-        // the table stays in global memory; nothing to stage
-        const unsigned long long ga = reinterpret_cast<unsigned long long>(gT);
-        C.tb[0] = static_cast<uint32_t>(ga);
-        C.tb[1] = static_cast<uint32_t>(ga >> 32);
-        C.thalf = 0u;
-        table_rows = 0;
-        if constexpr (kClusterTable<W>) {
-            asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        } else {
-            __syncthreads();
-        }
-    } else if constexpr (kClusterTable<W>) {
-        // this CTA's half of the table; the pair's halves are read through DSMEM
-        uint32_t rank;
-        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-        const uint32_t half = (static_cast<uint32_t>(P.K) + 1u) / 2u;
-        const uint32_t lo = rank * half, hi = min(static_cast<uint32_t>(P.K), lo + half);
-        for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) T[i - lo] = gT[i];
-        const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem));
-#pragma unroll
-        for (uint32_t r = 0; r < 2; ++r)
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(C.tb[r]) : "r"(local), "r"(r));
-        C.thalf = half;
-        table_rows = half;
-        // both halves staged before anyone reads across the pair
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t table_rows = 0;
+    if constexpr (kGlobalTable<W>) {
+        C.gt = gT;  // read in place (L2-resident, through L1)
     } else {
+        C.gt = nullptr;
         for (int i = threadIdx.x; i < P.K; i += blockDim.x) T[i] = gT[i];
-        C.tb[0] = C.tb[1] = 0u;
-        C.thalf = static_cast<uint32_t>(P.K);
+        table_rows = static_cast<uint32_t>(P.K);
         __syncthreads();
     }
     const uint32_t table_bytes = (table_rows * static_cast<uint32_t>(sizeof(Lmer<W>)) + 15u) / 16u * 16u;
@@ -2290,10 +2226,6 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
         }
     }
     __syncwarp();
-    if constexpr (kClusterTable<W>) {
-        // the partner CTA may still read this CTA's half of the table
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    }
     if (lane == 0) {
         const int map[W_N] = {C_PUSHES, C_VIABLE, C_SLOTS,    C_TUPLES,   C_LEAVES,     C_EMITTED,
                               C_VCMP,   C_NODES,  C_PAIR_REJ, C_TRI_REJ,  C_TASKS,      C_DONATED,
@@ -2339,11 +2271,9 @@ WarpPlan make_plan(int W, int l, int t) { return W == 1 ? make_plan_t<1>(l, t) :
 
 size_t node_bytes(int W) { return W == 1 ? sizeof(Node<1>) : sizeof(Node<2>); }
 
-int search_cluster(int W) { return W == 2 ? 2 : 1; }
-
 size_t search_smem(int W, int K, int warps, const WarpPlan& plan) {
-    // K == 0: the table stays in global memory
-    const size_t rows = (static_cast<size_t>(K) + search_cluster(W) - 1) / search_cluster(W);
+    // two-word builds read the table from global memory
+    const size_t rows = W == 2 ? 0 : static_cast<size_t>(K);
     return (rows * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
 }
 
@@ -2386,24 +2316,6 @@ cudaError_t set_search_smem(int W, int t, size_t bytes) {
     return cudaErrorInvalidValue;
 }
 
-// CTA pairs (2-CTA clusters) for the split two-word table
-cudaError_t launch_cluster(void (*kernel)(SearchParams), const SearchParams& P, int blocks, int warps, size_t smem,
-                           cudaStream_t s) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-    cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, P);
-}
-
 cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, size_t smem, cudaStream_t s) {
     const int mt = P.t < 2 ? 2 : P.t;
 #define PMS8G_CASE(WW, M)                                                 \
@@ -2414,7 +2326,6 @@ cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, s
                 return cudaGetLastError();                                \
             }                                                             \
         }                                                                 \
-        if constexpr (kClusterTable<WW>) return launch_cluster(search_kernel<WW, M, 16>, P, blocks, warps, smem, s); \
         search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P);     \
         return cudaGetLastError();                                        \
     }
