@@ -65,6 +65,8 @@ struct pms8g_ctx {
     std::string alphabet;
     pms8g_options opt{};
     std::vector<int32_t> anchors;
+    std::vector<int32_t> req_anchors;  // the caller's S1 offset list (context cache key)
+    std::string env_sig;                // creation-time test knobs (context cache key)
     std::vector<int32_t> task_ai;
     std::vector<uint32_t> task_u;
     int32_t* d_task_ai = nullptr;
@@ -168,6 +170,18 @@ void merge_scratch_free(MergeScratch& m) {
 }  // namespace pms8g
 
 namespace {
+
+// The environment knobs read when a context is created (test hooks): a cached
+// context is reused only under the same values.
+std::string env_signature() {
+    std::string sig;
+    for (const char* k : {"PMS8G_GLOBAL_TABLE", "PMS8G_NODE_CAP", "PMS8G_QCAP", "PMS8G_NO_TASK_ORDER"}) {
+        const char* v = std::getenv(k);
+        sig += v ? v : "-";
+        sig += '|';
+    }
+    return sig;
+}
 
 int alloc(pms8g_ctx* c, void** p, size_t bytes, char* err, size_t errlen) {
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
@@ -486,6 +500,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     c->K = n * c->w;
     c->t = t;
     c->ref_t = opt.threshold > 0 ? opt.threshold : pms8g_estimate_threshold(n, m, l, d, sigma);
+    c->env_sig = env_signature();
     c->opt = opt;
     c->device = dev;
     c->sms = prop.multiProcessorCount;
@@ -511,6 +526,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
             c->task_u.push_back(static_cast<uint32_t>(opt.branches[2 * i + 1]));
         }
     } else if (opt.anchors && opt.nanchors > 0) {
+        c->req_anchors.assign(opt.anchors, opt.anchors + opt.nanchors);
         for (int i = 0; i < opt.nanchors; ++i) {
             const int a = opt.anchors[i];
             if (a < 0 || a >= c->w) {
@@ -779,6 +795,7 @@ std::vector<pms8g_ctx*> g_batch;  // pms8g_solve_batch's lane contexts
 
 bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alphabet, const pms8g_options& o) {
     if (!c) return false;
+    if (c->env_sig != env_signature()) return false;
     const int dev = o.device;
     int cur = -1;
     if (dev < 0) cudaGetDevice(&cur);
@@ -786,7 +803,9 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
            c->opt.threshold == o.threshold && c->opt.sort_rows == o.sort_rows && c->opt.prune_level == o.prune_level &&
            c->opt.reverify == o.reverify && c->opt.max_motifs == o.max_motifs &&
            c->opt.shard_rank == o.shard_rank && std::max(1, c->opt.shard_count) == std::max(1, o.shard_count) &&
-           (dev < 0 ? cur : dev) == c->device && o.anchors == nullptr && o.branches == nullptr &&
+           (dev < 0 ? cur : dev) == c->device && o.branches == nullptr &&
+           (o.anchors == nullptr ? c->req_anchors.empty()
+                                 : c->req_anchors == std::vector<int32_t>(o.anchors, o.anchors + std::max(0, o.nanchors))) &&
            c->opt.warps_per_block == o.warps_per_block &&
            c->opt.blocks_per_sm == o.blocks_per_sm && c->opt.exact_tree == o.exact_tree && c->opt.queue == o.queue &&
            c->opt.grid_blocks == o.grid_blocks;
@@ -813,7 +832,7 @@ int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* al
         cached = true;
     } else {
         if ((rc = pms8g_ctx_create(n, m, l, d, alphabet, &opt, &c, err, errlen))) return rc;
-        if (!opt.anchors && !opt.branches) {
+        if (!opt.branches) {  // whole instances and S1 offset subsets (repeated by benchmarks) are cached
             pms8g_ctx_destroy(g_cache);
             g_cache = c;
             cached = true;
