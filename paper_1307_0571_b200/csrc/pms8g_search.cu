@@ -567,7 +567,6 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     uint32_t e_next2 = kPipeV ? load_entry(lane + 32) : 0u;
     Lmer<W> V_next;
     if constexpr (kPipeV) V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
-#pragma unroll(MT >= 4 ? 2 : 1)
     for (int base = 0; base < n_iter; base += 32) {
         const int f = base + lane;
         const bool valid = f < n_iter;
