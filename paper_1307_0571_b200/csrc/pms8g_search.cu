@@ -76,7 +76,9 @@ struct WarpFixed {
     uint32_t fsm[MAXT][4];
     uint32_t fmiu[MAXT][2];
     int32_t fhs[MAXT];
-    uint32_t cons[MAXT + 1][9];  // consensus row rule: slot k = masks of stack[0..k-1] (cons_prepare)
+    // consensus row rule: slot k = masks of stack[0..k-1] (cons_prepare);
+    // 12-word (16-byte aligned) slots so a filter loads them with LDS.128
+    __align__(16) uint32_t cons[MAXT + 1][12];
 };
 
 
@@ -354,7 +356,18 @@ __device__ __forceinline__ ConsMasks<W> load_cons(const WarpCtx<W, MT>& C, int k
 
 template <int W>
 __device__ __forceinline__ bool cons_pass(const ConsMasks<W>& cm, const Lmer<W>& x) {
-    const uint32_t* g = cm.slot;
+    // the 4W masks and `need` as LDS.128/LDS.64 broadcasts
+    uint32_t g[4 * W + 1];
+    const uint4* v = reinterpret_cast<const uint4*>(cm.slot);
+    if constexpr (W == 2) {
+        const uint4 a = v[0], b = v[1];
+        g[0] = a.x, g[1] = a.y, g[2] = a.z, g[3] = a.w, g[4] = b.x, g[5] = b.y, g[6] = b.z, g[7] = b.w;
+        g[8] = cm.slot[8];
+    } else {
+        const uint4 a = v[0];
+        g[0] = a.x, g[1] = a.y, g[2] = a.z, g[3] = a.w;
+        g[4] = cm.slot[4];
+    }
     int matches = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -582,6 +595,8 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             if (valid) V = tr.get(e & ID_MASK);
         }
         bool keep = false;
+        Mask<W> mu;
+        int hvu = 0;
         if (valid) {
             // the consensus rule first: at deep levels it rejects most slots
             keep = true;
@@ -589,14 +604,25 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 keep = cons_pass<W>(cm, V);
                 cons_rej += !keep;
             }
-            Mask<W> mu;
-            int hvu = 0;
             if (keep) {
                 mu = mism<W>(V, U);
                 hvu = popcm<W>(mu);
                 keep = hvu <= two_d;
                 pair_rej += !keep;
             }
+        }
+        if constexpr (MT >= 5) {
+            // Theorem 1 against the older members: skipped by the whole warp
+            // when no lane survived the cheap rules (most blocks at depth;
+            // measured +3.5% on (50,21), -4% on the t = 4 builds, which keep
+            // the unrolled form)
+            if (__any_sync(0xffffffffu, keep)) {
+                const bool before = keep;
+                for (int i = 0; i < k; ++i)
+                    if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
+                tri_rej += before && !keep;
+            }
+        } else {
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 if (i < k && keep) {
@@ -606,15 +632,18 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
-        out += __popc(bal);
-        // per-row kept counts: one leader lane per distinct row of the block
-        // (rows are contiguous segments, so a block spans one or two rows)
-        const uint32_t row = e >> 24;
-        const unsigned grp = __match_any_sync(0xffffffffu, row);
-        if (valid && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint16_t>(__popc(bal & grp));
-        __syncwarp();
+        if (MT < 5 || bal) {  // warp-uniform: deep blocks without survivors write nothing
+            if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
+            out += __popc(bal);
+            // per-row kept counts: one leader lane per distinct row among the
+            // kept entries (rows are contiguous segments: one or two per block)
+            const uint32_t row = e >> 24;
+            const unsigned grp = __match_any_sync(0xffffffffu, row) & bal;
+            if (keep && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint16_t>(__popc(grp));
+            __syncwarp();
+        }
     }
+    __syncwarp();
     // an emptied row is detected after the pass (almost every push is viable,
     // so the pass rarely could have stopped early)
     C.add(W_PUSH, 1);
@@ -707,6 +736,8 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     for (int base = 0; base < cnt; base += 32) {
         const int f = base + lane;
         bool keep = false;
+        Mask<W> mu;
+        int hvu = 0;
         const uint32_t e = e_next;
         Lmer<W> V;
         if constexpr (kPipeV) {
@@ -720,13 +751,17 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
         }
         if (f < cnt) {
             keep = !cons || cons_pass<W>(cm, V);
-            Mask<W> mu;
-            int hvu = 0;
             if (keep) {
                 mu = mism<W>(V, U);
                 hvu = popcm<W>(mu);
                 keep = hvu <= two_d;
             }
+        }
+        if constexpr (MT >= 5) {
+            if (__any_sync(0xffffffffu, keep))  // as filter_push: whole-warp skip
+                for (int i = 0; i < k; ++i)
+                    if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
+        } else {
 #pragma unroll
             for (int i = 0; i < MT; ++i)
                 if (i < k && keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
