@@ -22,6 +22,8 @@
 //   branch l d seed anchor "i1,i2,.." [t]  -> motif set of depth-1 branches (anchor, row[i])
 //   stats  l d seed "o1,.." [t]            -> per-depth work counters (mirrors recurse())
 //   branchtime l d seed threads jobs cap [t] -> capped depth-1 branch sample (CPU baseline, (50,21))
+//   branch2 l d seed t threads             -> planted depth-1 branch split into depth-2 branches (union)
+//   anchorsplit l d seed t threads "o1,.." -> whole S1 l-mers, depth-1 branches of all in one dynamic loop
 //   kat                                    -> SPEC known-answer values as JSON
 //   file   path l d threads [t alphabet]   -> solve sequences read from a file (one per line)
 #include <omp.h>
@@ -361,6 +363,177 @@ int cmd_branch(int argc, char** argv) {
     return 0;
 }
 
+// The planted depth-1 branch of the planted S1 l-mer, split into its depth-2
+// branches (anchor, u1, u2) run by an OpenMP dynamic loop: the union of the
+// depth-2 motif sets is the depth-1 branch's set (every branching-row l-mer is
+// branched on, src/solver.cpp:406-419). For (l,d) where one depth-1 branch
+// takes hours of one core ((50,21)). Prints one DONE line per depth-2 branch
+// to stderr (progress) and the union on stdout.
+int cmd_branch2(int argc, char** argv) {
+    const int l = std::atoi(argv[2]), d = std::atoi(argv[3]);
+    const uint64_t seed = std::strtoull(argv[4], nullptr, 10);
+    const int t = std::atoi(argv[5]);
+    const int threads = std::atoi(argv[6]);
+    const auto inst = make(l, d, seed);
+    SolverContext ctx(inst.problem, config_with(t));
+    const auto& set = ctx.set();
+    const uint32_t a = set.lmer_id(0, static_cast<uint32_t>(inst.positions[0]));
+    auto setup = [&](MotifSearch& s) -> bool {
+        auto& rw = const_cast<RowMatrix&>(s.rows());
+        rw.reset_full();
+        rw.restrict_row(0, a);
+        rw.sort_rows_by_size(0);
+        if (!s.push(a)) return false;
+        rw.sort_rows_by_size(1);
+        return true;
+    };
+    uint32_t u1 = 0;
+    std::vector<uint32_t> brow2;
+    {
+        MotifSearch s(ctx);
+        if (!setup(s)) {
+            std::printf("ANCHOR_NOT_VIABLE\n");
+            return 0;
+        }
+        bool found = false;
+        for (uint32_t u : s.rows().live(s.rows().row_at_position(1))) {
+            const auto r = set.ref_of(u);
+            if (static_cast<int>(r.offset) == inst.positions[r.seq]) {
+                u1 = u;
+                found = true;
+                break;
+            }
+        }
+        if (!found || !s.push(u1)) {
+            std::printf("PLANTED_BRANCH_NOT_VIABLE\n");
+            return 0;
+        }
+        const_cast<RowMatrix&>(s.rows()).sort_rows_by_size(2);
+        const auto live = s.rows().live(s.rows().row_at_position(2));
+        brow2.assign(live.begin(), live.end());
+        const auto r1 = set.ref_of(u1);
+        std::printf("BRANCH1 anchor=%d u1_seq=%u u1_off=%u row2=%d size=%zu threshold=%d\n", inst.positions[0],
+                    r1.seq, r1.offset, s.rows().row_at_position(2), brow2.size(), ctx.threshold());
+        std::fflush(stdout);
+    }
+    std::vector<std::vector<std::string>> res(brow2.size());
+    std::atomic<long> next{0};
+    const double t0 = now();
+#pragma omp parallel num_threads(threads)
+    {
+        MotifSearch s(ctx);
+        for (;;) {
+            const long j = next.fetch_add(1);
+            if (j >= static_cast<long>(brow2.size())) break;
+            const double b = now();
+            if (setup(s)) {
+                auto& rw = const_cast<RowMatrix&>(s.rows());
+                if (s.push(u1)) {
+                    rw.sort_rows_by_size(2);
+                    if (s.push(brow2[static_cast<size_t>(j)])) {
+                        rw.sort_rows_by_size(3);
+                        Stats st(ctx.threshold());
+                        if (s.depth() == ctx.threshold()) s.enumerate_and_collect(res[j]);
+                        else stats_recurse(ctx, s, st, res[j]);
+                    }
+                    s.pop();
+                }
+                s.pop();
+            }
+            while (s.depth() > 0) s.pop();
+            const auto r = set.ref_of(brow2[static_cast<size_t>(j)]);
+            std::fprintf(stderr, "DONE %ld/%zu seq=%u off=%u %.3f s (elapsed %.1f s) motifs=%zu\n", j,
+                         brow2.size(), r.seq, r.offset, now() - b, now() - t0, res[j].size());
+        }
+    }
+    std::vector<std::string> all;
+    for (auto& v : res) all.insert(all.end(), v.begin(), v.end());
+    const auto ms = canonical_motif_set(all);
+    std::printf("UNION %.3f", now() - t0);
+    for (const auto& m : ms) std::printf(" %s", m.c_str());
+    std::printf("\n");
+    return 0;
+}
+
+// Whole S1 l-mers (run_anchored, src/solver.cpp:427-432), each split into its
+// depth-1 branches, all branches of all listed S1 offsets in one OpenMP
+// dynamic loop (one heavy S1 l-mer then uses every thread). Prints one
+// ANCHOR line per offset: offset, thread-seconds, motif set.
+int cmd_anchorsplit(int argc, char** argv) {
+    const int l = std::atoi(argv[2]), d = std::atoi(argv[3]);
+    const uint64_t seed = std::strtoull(argv[4], nullptr, 10);
+    const int t = std::atoi(argv[5]);
+    const int threads = std::atoi(argv[6]);
+    const auto offsets = parse_list(argv[7]);
+    const auto inst = make(l, d, seed);
+    SolverContext ctx(inst.problem, config_with(t));
+    const auto& set = ctx.set();
+    auto setup = [&](MotifSearch& s, uint32_t a) -> bool {
+        auto& rw = const_cast<RowMatrix&>(s.rows());
+        rw.reset_full();
+        rw.restrict_row(0, a);
+        rw.sort_rows_by_size(0);
+        if (!s.push(a)) return false;
+        rw.sort_rows_by_size(1);
+        return true;
+    };
+    struct Job {
+        size_t ai;
+        uint32_t u;
+    };
+    std::vector<Job> jobs;
+    {
+        MotifSearch s(ctx);
+        for (size_t i = 0; i < offsets.size(); ++i) {
+            const uint32_t a = set.lmer_id(0, static_cast<uint32_t>(offsets[i]));
+            if (setup(s, a))
+                for (uint32_t u : s.rows().live(s.rows().row_at_position(1))) jobs.push_back({i, u});
+            while (s.depth() > 0) s.pop();
+        }
+    }
+    std::vector<std::vector<std::string>> res(offsets.size());
+    std::vector<double> secs(offsets.size(), 0.0);
+    std::atomic<long> next{0};
+    const double t0 = now();
+#pragma omp parallel num_threads(threads)
+    {
+        MotifSearch s(ctx);
+        std::vector<std::string> out;
+        for (;;) {
+            const long j = next.fetch_add(1);
+            if (j >= static_cast<long>(jobs.size())) break;
+            const double b = now();
+            const Job jb = jobs[static_cast<size_t>(j)];
+            out.clear();
+            if (setup(s, set.lmer_id(0, static_cast<uint32_t>(offsets[jb.ai])))) {
+                if (s.push(jb.u)) {
+                    const_cast<RowMatrix&>(s.rows()).sort_rows_by_size(2);
+                    Stats st(ctx.threshold());
+                    if (s.depth() == ctx.threshold()) s.enumerate_and_collect(out);
+                    else stats_recurse(ctx, s, st, out);
+                }
+            }
+            while (s.depth() > 0) s.pop();
+            const double dt = now() - b;
+#pragma omp critical
+            {
+                secs[jb.ai] += dt;
+                res[jb.ai].insert(res[jb.ai].end(), out.begin(), out.end());
+            }
+            if (j % 500 == 0) std::fprintf(stderr, "job %ld/%zu elapsed %.1f s\n", j, jobs.size(), now() - t0);
+        }
+    }
+    for (size_t i = 0; i < offsets.size(); ++i) {
+        const auto ms = canonical_motif_set(res[i]);
+        std::printf("ANCHOR %ld %.6f", offsets[i], secs[i]);
+        for (const auto& m : ms) std::printf(" %s", m.c_str());
+        std::printf("\n");
+    }
+    std::printf("TIMING {\"wall_seconds\": %.6f, \"jobs\": %zu, \"threads\": %d, \"threshold\": %d}\n", now() - t0,
+                jobs.size(), threads, ctx.threshold());
+    return 0;
+}
+
 // recurse (src/solver.cpp:406-419) through the public push/pop/rows API like
 // stats_recurse, giving up once `deadline` passes (the subtree is then only
 // partly searched: its time is a lower bound). Returns false on timeout.
@@ -652,6 +825,8 @@ int main(int argc, char** argv) {
         if (cmd == "anchors" && argc >= 7) return cmd_anchors(argc, argv);
         if (cmd == "time" && argc >= 7) return cmd_time(argc, argv);
         if (cmd == "branch" && argc >= 7) return cmd_branch(argc, argv);
+        if (cmd == "branch2" && argc >= 7) return cmd_branch2(argc, argv);
+        if (cmd == "anchorsplit" && argc >= 8) return cmd_anchorsplit(argc, argv);
         if (cmd == "stats" && argc >= 6) return cmd_stats(argc, argv);
         if (cmd == "branchtime" && argc >= 8) return cmd_branchtime(argc, argv);
         if (cmd == "kat") return cmd_kat();

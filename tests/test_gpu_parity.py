@@ -253,21 +253,23 @@ def _branch_parity(name):
 
 def test_branch_sample_50_21():
     # two-word (l=50) path at full size, t from the GPU rule: depth-1 branches
-    # of S1 l-mer 0 as the reference computed them
+    # of S1 l-mer 0 and the planted depth-1 branch as the reference computed
+    # them; the planted one is non-empty, so an all-empty output fails
     _branch_parity("branches_50_21.json")
+    _branch_parity("branches_50_21_planted.json")
+    sets = [b["motifs"] for name in ("branches_50_21.json", "branches_50_21_planted.json")
+            for sample in golden(name) for b in sample["branches"]]
+    assert any(sets)
 
 
 def test_branch_planted_50_21():
     # the depth-1 branch (planted occurrence of sequence 0, planted occurrence
-    # in its branching row): the reference needs hours of CPU for it, so when
-    # its golden is absent the check is size-independent: the planted motif
+    # in its branching row) given as 19 candidate branches, size-independent
+    # checks: the planted motif
     # is a common d-neighbour of a tuple of planted occurrences, all of which
     # survive every filter, so it must be emitted under this branch, and every
     # emitted motif must be a motif of the instance (CPU oracle check)
-    path = os.path.join(ROOT, "tests", "golden", "branches_50_21_planted.json")
-    if os.path.exists(path):
-        _branch_parity("branches_50_21_planted.json")
-        return
+    # reference-pinned by branches_50_21_planted.json (test_branch_sample_50_21)
     inst = planted(50, 21, 1)
     pos = list(inst.positions)
     br = [(pos[0], s, pos[s]) for s in range(1, 20)]  # only the branching-row one is a branch
