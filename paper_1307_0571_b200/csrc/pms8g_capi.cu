@@ -232,8 +232,7 @@ int validate_problem(int n, int m, int l, int d, const char* alphabet, char* err
                 return fail(err, errlen, PMS8G_ERR_INVALID, "duplicate alphabet symbol '%c'", alphabet[i]);
     // GPU path limits: 2 bit planes up to 4 symbols (l <= 64),
     // B = ceil(log2 sigma) planes of one word up to 32 symbols (l <= 32 and
-    // B*l <= 128 key bits), 32 rows per warp table, 24-bit l-mer ids, 16-bit
-    // row offsets
+    // B*l <= 128 key bits), 32 rows per warp table, 24-bit l-mer ids
     if (s > 32)
         return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports alphabets of at most 32 symbols, got %d", s);
     if (s <= 4 && l > 64) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports l <= 64, got %d", l);
@@ -247,7 +246,9 @@ int validate_problem(int n, int m, int l, int d, const char* alphabet, char* err
     }
     if (n > MAXN) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n <= %d sequences, got %d", MAXN, n);
     const long long K = static_cast<long long>(n) * (m - l + 1);
-    if (K > 65535) return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n*(m-l+1) <= 65535, got %lld", K);
+    if (K > static_cast<long long>(ID_MASK))
+        return fail(err, errlen, PMS8G_ERR_INVALID, "GPU path supports n*(m-l+1) <= %u (24-bit l-mer ids), got %lld",
+                    ID_MASK, K);
     *sigma = s;
     return PMS8G_OK;
 }

@@ -23,8 +23,8 @@ struct Lmer {
 
 // Row table of one level: rows in physical storage order.
 struct LevelMeta {
-    uint16_t start[MAXN];
-    uint16_t cnt[MAXN];
+    uint32_t start[MAXN];
+    uint32_t cnt[MAXN];
     uint8_t order[MAXN];  // row id at physical position j
     int32_t nrows;
     int32_t total;
@@ -58,6 +58,7 @@ enum Ctr {
     C_TLN = C_LOG0 + 256,            // diagnostics: timeline records written
     C_STATIC,                        // static tasks claimed by this device
     C_CONS_REJ,                      // slots rejected by the stack consensus row rule
+    C_ROUNDS,                        // enumeration rounds (a round pops up to 16 nodes)
     C_NCTR
 };
 

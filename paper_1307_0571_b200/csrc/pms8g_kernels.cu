@@ -119,8 +119,8 @@ __global__ void rowbuild_kernel(const Lmer<W>* __restrict__ table, int n, int w,
         const bool any_empty = __any_sync(0xffffffffu, empty);
         LevelMeta* M = l1_meta + ai;
         if (lane < nrows) {
-            M->start[lane] = static_cast<uint16_t>(excl);
-            M->cnt[lane] = static_cast<uint16_t>(cpos);
+            M->start[lane] = static_cast<uint32_t>(excl);
+            M->cnt[lane] = static_cast<uint32_t>(cpos);
             int row = 0;
             for (int q = 1; q < n; ++q)
                 if (posof[q] == lane) row = q;

@@ -44,7 +44,7 @@ struct NodeSmem {
 };
 
 enum WCtr { W_PUSH, W_VIABLE, W_SLOTS, W_TUPLES, W_LEAVES, W_EMIT, W_VCMP, W_NODES, W_PAIRREJ, W_TRIREJ, W_TASKS,
-            W_DONATED, W_REPLAYS, W_CLKF, W_CLKP, W_CONSREJ, W_N };
+            W_DONATED, W_REPLAYS, W_CLKF, W_CLKP, W_CONSREJ, W_ROUNDS, W_N };
 
 // Wait state of a warp's claim loop (lane 0 only; shared memory, so the
 // persistent loop keeps no registers for it).
@@ -61,7 +61,7 @@ struct WarpFixed {
     int iter[MAXT + 1];
     int iter_end[MAXT + 1];
     uint32_t stack_id[MAXT];
-    uint16_t cnt_by_row[MAXN];
+    uint32_t cnt_by_row[MAXN];
     uint8_t vorder[MAXN];
     uint8_t perm[64];            // enumeration depth -> l-mer position of the current tuple
     unsigned long long diag[5];  // diagnostics: counters at task start + start time (ns)
@@ -213,6 +213,15 @@ __device__ __noinline__ void jitter_sleep(const SearchParams& P, unsigned long l
         __nanosleep(step);
         ns -= step;
     }
+}
+
+// The tuple size of a build: builds are specialised on the switch depth
+// (launch_search picks MT = max(2, t)), so t == MT whenever MT >= 3 and only
+// the MT = 2 build sees two sizes (t = 1, 2). Folding t into a constant drops
+// the per-member predicates and the code of the smaller sizes.
+template <int MT>
+__device__ __forceinline__ int tuple_size(int t) {
+    return MT >= 3 ? MT : t;
 }
 
 // ---------------------------------------------------------------- static tasks
@@ -639,7 +648,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             // kept entries (rows are contiguous segments: one or two per block)
             const uint32_t row = e >> 24;
             const unsigned grp = __match_any_sync(0xffffffffu, row) & bal;
-            if (keep && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint16_t>(__popc(grp));
+            if (keep && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint32_t>(__popc(grp));
             __syncwarp();
         }
     }
@@ -687,8 +696,8 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 key = __shfl_sync(0xffffffffu, key, 0);
             }
             if (lane < nr2) {
-                Ld.start[lane] = static_cast<uint16_t>(incl - c);
-                Ld.cnt[lane] = static_cast<uint16_t>(c);
+                Ld.start[lane] = static_cast<uint32_t>(incl - c);
+                Ld.cnt[lane] = static_cast<uint32_t>(c);
                 Ld.order[lane] = row;
             }
             if (lane == 0) {
@@ -795,7 +804,7 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
         const int j = lane < jb ? lane : lane + 1;
         Ld.start[lane] = Ls.start[j];
         c = Ls.cnt[j];
-        Ld.cnt[lane] = static_cast<uint16_t>(c);
+        Ld.cnt[lane] = static_cast<uint32_t>(c);
         Ld.order[lane] = Ls.order[j];
     }
     // smallest unfiltered row (ties by position)
@@ -819,7 +828,7 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
         const int pk = p < jb ? p : p + 1;
         const int got = filter_one_row<W, MT>(C, k, pk);
         if (lane == 0) {
-            Ld.cnt[p] = static_cast<uint16_t>(got);
+            Ld.cnt[p] = static_cast<uint32_t>(got);
             S.lazy_mask = 1u << p;
         }
         __syncwarp();
@@ -1009,7 +1018,7 @@ __device__ __forceinline__ void ensure_row(WarpCtx<W, MT>& C, int t, int p) {
     const int pk = p < jb ? p : p + 1;
     const int got = filter_one_row<W, MT>(C, k, pk);
     if (C.lane == 0) {
-        S.lev[t].cnt[p] = static_cast<uint16_t>(got);
+        S.lev[t].cnt[p] = static_cast<uint32_t>(got);
         S.lazy_mask |= 1u << p;
     }
     __syncwarp();
@@ -1063,6 +1072,19 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
     __syncwarp();
 }
 
+// Verification order of a level's rows: S.vorder[r] = position of the r-th
+// smallest row (ties by position), verify_candidate's ascending-size order
+// (src/solver.cpp:344-362). A rolled loop over register broadcasts: it runs
+// once per tuple, and unrolled it cost ~5 KB of hot code (I-cache).
+__device__ __forceinline__ void rank_rows(WarpFixed& S, const LevelMeta& L, int lane) {
+    const int nr = L.nrows;
+    const unsigned key = lane < nr ? (static_cast<unsigned>(L.cnt[lane]) << 5) | static_cast<unsigned>(lane) : ~0u;
+    int rank = 0;
+#pragma unroll 1
+    for (int q = 0; q < nr; ++q) rank += __shfl_sync(0xffffffffu, key, q) < key;
+    if (lane < nr) S.vorder[rank] = static_cast<uint8_t>(lane);
+}
+
 // ---------------------------------------------------------------- enumeration
 // Enumeration order of the tuple's positions. The common d-neighbourhood
 // does not depend on the order in which positions are assigned, and the
@@ -1078,6 +1100,7 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
 // the natural order (the reference's tree).
 template <int W, int MT>
 __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* Tm) {
+    t = tuple_size<MT>(t);
     const int lane = C.lane, l = C.P->l;
     WarpFixed& S = *C.S();
     constexpr int NC = W;  // 32-position chunks
@@ -1181,6 +1204,7 @@ __device__ __noinline__ void order_positions(WarpCtx<W, MT>& C, int t, Lmer<W>* 
 // the consensus suffix bound, plus the verification row order.
 template <int W, int MT>
 __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const LevelMeta& L, Lmer<W>* Tm) {
+    t = tuple_size<MT>(t);
     const SearchParams& P = *C.P;
     const int lane = C.lane, l = P.l;
     WarpFixed& S = *C.S();
@@ -1249,15 +1273,7 @@ __device__ __noinline__ void prepare_tuple(WarpCtx<W, MT>& C, int t, const Level
         if (p <= l) gen_cons(C)[p] = static_cast<uint8_t>(incl + carry);
         carry += __shfl_sync(0xffffffffu, incl, 0);
     }
-    if (lane < L.nrows) {
-        const int c = L.cnt[lane];
-        int rank = 0;
-        for (int q = 0; q < L.nrows; ++q) {
-            const int cq = L.cnt[q];
-            rank += (cq < c) || (cq == c && q < lane);
-        }
-        S.vorder[rank] = static_cast<uint8_t>(lane);
-    }
+    rank_rows(S, L, lane);
     __syncwarp();
 }
 
@@ -1344,6 +1360,7 @@ __device__ __forceinline__ bool bytes_ge(uint32_t x, uint32_t y) {
 
 template <int W, int MT>
 __device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const LevelMeta& L, const Lmer<W>* Tm) {
+    t = tuple_size<MT>(t);
     const int lane = C.lane, l = C.P->l;
     WarpFixed& S = *C.S();
     uint32_t* dec = reinterpret_cast<uint32_t*>(C.thr());          // [l][4]
@@ -1441,15 +1458,7 @@ __device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const 
             thr[p] = w;
         }
     }
-    if (lane < L.nrows) {
-        const int c = L.cnt[lane];
-        int rank = 0;
-        for (int q = 0; q < L.nrows; ++q) {
-            const int cq = L.cnt[q];
-            rank += (cq < c) || (cq == c && q < lane);
-        }
-        S.vorder[rank] = static_cast<uint8_t>(lane);
-    }
+    rank_rows(S, L, lane);
     __syncwarp();
 }
 
@@ -1461,6 +1470,7 @@ __device__ __noinline__ void prepare_tuple_swar(WarpCtx<W, MT>& C, int t, const 
 // order is a stable rank over at most five (cost, distinct) classes.
 template <int MT>
 __device__ __noinline__ void prepare_tuple_fast(WarpCtx<1, MT>& C, int t, const LevelMeta& L, Lmer<1>* Tm) {
+    t = tuple_size<MT>(t);
     const int lane = C.lane, l = C.P->l;
     WarpFixed& S = *C.S();
     uint4* dec4 = reinterpret_cast<uint4*>(C.thr());                       // [l] x {c = 0..3}
@@ -1574,15 +1584,7 @@ __device__ __noinline__ void prepare_tuple_fast(WarpCtx<1, MT>& C, int t, const 
         w.w = q == 0 ? 0u : static_cast<uint32_t>(q < 32 ? prevpos : lastpos);  // position of depth q - 1
         thr[q] = w;
     }
-    if (lane < L.nrows) {
-        const int c = L.cnt[lane];
-        int rank = 0;
-        for (int q = 0; q < L.nrows; ++q) {
-            const int cq = L.cnt[q];
-            rank += (cq < c) || (cq == c && q < lane);
-        }
-        S.vorder[rank] = static_cast<uint8_t>(lane);
-    }
+    rank_rows(S, L, lane);
     __syncwarp();
 }
 
@@ -1679,7 +1681,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     const int cand_cap = P.plan.cand_cap;
     const uint32_t odd = lane & 1;
     unsigned long long leaves = 0, nodes = 0;
-    uint32_t leaves32 = 0, nodes32 = 0;
+    uint32_t leaves32 = 0, nodes32 = 0, rounds32 = 0;
     int rounds = 0, burst = 0;
     int ncand = 0;
     const bool may_donate = P.donate != 0;
@@ -1744,6 +1746,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
         const int take = min(16, nn);
         const int base = nn - take;
         const bool active = (lane >> 1) < take;
+        ++rounds32;
         uint4 nd = make_uint4(0u, 0u, 0u, 0u);
         if (active) nd = ns[(bot + base + (lane >> 1)) & (NS - 1)];
         nodes32 += take;
@@ -1794,6 +1797,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
     }
     leaves += leaves32;
     nodes += nodes32;
+    C.add(W_ROUNDS, rounds32);
     if (ncand > 0) verify_all<1, MT>(C, L, entries, ncand);
     nodes_out += nodes;
     leaves_out += leaves;
@@ -1841,6 +1845,7 @@ __device__ __forceinline__ bool stack_consensus_ok(const WarpCtx<W, MT>& C, int 
 // copied to the bottom of the node stack.
 template <int W, int MT>
 __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon) {
+    t = tuple_size<MT>(t);
     const SearchParams& P = *C.P;
     const int lane = C.lane;
     WarpFixed& S = *C.S();
@@ -2264,7 +2269,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     if (lane == 0) {
         const int map[W_N] = {C_PUSHES, C_VIABLE, C_SLOTS,    C_TUPLES,   C_LEAVES,     C_EMITTED,
                               C_VCMP,   C_NODES,  C_PAIR_REJ, C_TRI_REJ,  C_TASKS,      C_DONATED,
-                              C_REPLAYS, C_CLK_FILTER, C_CLK_PATTERN, C_CONS_REJ};
+                              C_REPLAYS, C_CLK_FILTER, C_CLK_PATTERN, C_CONS_REJ, C_ROUNDS};
 #pragma unroll
         for (int i = 0; i < W_N; ++i) atomicAdd(P.counters + map[i], S.ctr[i]);
     }

@@ -142,8 +142,8 @@ __global__ void rowbuild_sigma_kernel(const LmerS<B>* __restrict__ table, int n,
         const bool any_empty = __any_sync(0xffffffffu, lane < nrows && cpos == 0);
         LevelMeta* M = l1_meta + ai;
         if (lane < nrows) {
-            M->start[lane] = static_cast<uint16_t>(incl - cpos);
-            M->cnt[lane] = static_cast<uint16_t>(cpos);
+            M->start[lane] = static_cast<uint32_t>(incl - cpos);
+            M->cnt[lane] = static_cast<uint32_t>(cpos);
             M->order[lane] = static_cast<uint8_t>(row);
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
@@ -178,7 +178,7 @@ struct SigmaWarp {
     LevelMeta lev[MAXT + 1];
     int iter[MAXT + 1], iter_end[MAXT + 1];
     uint32_t stack_id[MAXT];
-    uint16_t cnt_by_row[MAXN];
+    uint32_t cnt_by_row[MAXN];
     uint8_t sym[MAXT][32];           // tuple members' symbols per position
     uint8_t pair_suf[33][NPAIR];     // Hd of members i<j over positions >= q
     uint8_t cons_suf[33];            // consensus cost over positions >= q
@@ -272,7 +272,7 @@ __device__ __noinline__ bool sigma_push(SCtx<B, MT>& C, int k) {
             kept += __popc(bal);
         }
         slots += static_cast<unsigned long long>(cnt);
-        if (lane == 0) S.cnt_by_row[row] = static_cast<uint16_t>(kept);
+        if (lane == 0) S.cnt_by_row[row] = static_cast<uint32_t>(kept);
         out += kept;
     }
     __syncwarp();
@@ -297,8 +297,8 @@ __device__ __noinline__ bool sigma_push(SCtx<B, MT>& C, int k) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, s));
     if (lane < nr2) {
-        Ld.start[lane] = static_cast<uint16_t>(incl - c);
-        Ld.cnt[lane] = static_cast<uint16_t>(c);
+        Ld.start[lane] = static_cast<uint32_t>(incl - c);
+        Ld.cnt[lane] = static_cast<uint32_t>(c);
         Ld.order[lane] = static_cast<uint8_t>(row);
     }
     if (lane == 0) {

@@ -47,5 +47,7 @@ if len(c) > 55:
               f"nodes={r[6]} prologue_cycles={r[7]}")
     print(f"  idle warp-cycles {c[55]:.3e} busy(filter+pattern) {c[8] + c[9]:.3e}"
           + (f" of {tot:.3e} available: idle {c[55] / tot:.1%}" if tot else ""))
+if len(c) > 396 and c[396]:
+    print(f"  enumeration rounds {c[396]} nodes/round {c[7] / c[396]:.2f} (fast loop, up to 16)")
 print("  task cycles histogram (log2 bucket: count): " +
       " ".join(f"{i}:{v}" for i, v in enumerate(hist) if v))
