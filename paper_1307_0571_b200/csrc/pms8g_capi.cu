@@ -109,7 +109,7 @@ struct pms8g_ctx {
     QueueState* d_qs = nullptr;
     unsigned int* d_qstate = nullptr;
     uint8_t* d_qslots = nullptr;
-    int qcap = 0, qslot_bytes = 0;
+    int qcap = 0, qslot_bytes = 0, don_cap = 0;
     size_t device_bytes = 0;
     long long unique_count = 0;
     pms8g_report report{};
@@ -399,11 +399,13 @@ int pms8g_gpu_threshold(int n, int m, int l, int d, int sigma) {
         const double ls = std::log(static_cast<double>(n)) + std::log(static_cast<double>(l)) + mx + std::log(sum);
         const double lp = terms[t - 1] + log_nd + (t - 1) * log_q + std::log(static_cast<double>(l));
         if (lp - ls <= beta) {
-            // 5+ member tuples without a common neighbour are rejected by the
-            // root consensus bound before their tables are built, so one level
-            // deeper pays there ((50,21): t=6 31.8 s vs t=5 62.2 s for S1
-            // l-mer 0, 29.0 vs 34.8 s per S1 l-mer over 8)
-            if (t >= 5 && t < MAXT && t < n) ++t;
+            // where the model asks for 5+ members the tuples' neighbourhoods are
+            // still huge and heavy-tailed (one (50,21) 6-tuple kept 300+ warps
+            // busy for 0.4 s); the push filters with the consensus row rule are
+            // cheap there, so two levels deeper pay: (50,21) per 56 S1 l-mers
+            // t=5 minutes, t=6 1.28 s (22,269 tuples, 2.3 G nodes), t=7 0.49 s
+            // (247 tuples, 4.3 M nodes)
+            if (t >= 5) t = std::min(std::min(t + 2, MAXT), n);
             return t;
         }
     }
@@ -629,7 +631,11 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     }
     c->qcap = 8192;
     if (const char* q = std::getenv("PMS8G_QCAP")) c->qcap = std::max(16, std::atoi(q));  // ring stress tests
-    c->qslot_bytes = static_cast<int>(task_slot_bytes(c->W));
+    // level hand-off with donated tasks (TaskHeader::hlevel): only searches
+    // with t >= 3 have a level >= 2 to hand off
+    c->don_cap = t >= 3 ? std::min(c->level_cap, 16384) : 0;
+    if (const char* q = std::getenv("PMS8G_DON_CAP")) c->don_cap = std::max(0, std::min(c->level_cap, std::atoi(q)));
+    c->qslot_bytes = static_cast<int>(task_slot_bytes(c->W, c->don_cap));
     AL(c->d_qs, sizeof(QueueState));
     AL(c->d_qslots, static_cast<size_t>(c->qcap) * c->qslot_bytes);
     AL(c->d_qstate, sizeof(unsigned int) * c->qcap);
@@ -1249,10 +1255,16 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             P.qstate = c->d_qstate;
             P.qcap = c->qcap;
             P.qslot_bytes = c->qslot_bytes;
+            P.don_cap = c->don_cap;
+            P.qslot_lvl_off = static_cast<int>(task_slot_level_offset(c->W));
             P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
             P.don_pushes = 32;  // DFS pushes between starvation checks (4: +1.8 % on (17,6), +1.6 % (21,8))
             P.don_rounds_mask = 63;
             P.don_burst = 1;
+            // generic (two-word / t >= 5) enumeration: a check per round measured slower
+            // ((50,21) t=6: 1.89 s vs 1.29 s per 56 S1 l-mers; the node batches get too small)
+            P.don_gen_mask = 7;
+            if (const char* e = std::getenv("PMS8G_DON_GEN")) P.don_gen_mask = std::max(1, std::atoi(e)) - 1;
             if (const char* e = std::getenv("PMS8G_DON_BURST")) P.don_burst = std::max(1, std::atoi(e));
             if (const char* e = std::getenv("PMS8G_DON_PUSHES")) P.don_pushes = std::max(1, std::atoi(e));
             if (const char* e = std::getenv("PMS8G_LOG_CYCLES")) P.log_cycles = std::atoll(e);

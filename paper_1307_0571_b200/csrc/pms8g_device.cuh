@@ -6,7 +6,7 @@
 
 namespace pms8g {
 
-constexpr int MAXT = 6;   // deepest switch depth (stack size at enumeration)
+constexpr int MAXT = 7;   // deepest switch depth (stack size at enumeration)
 constexpr int MAXN = 32;  // rows (sequences) handled by one warp's row tables
 constexpr int NPAIR = MAXT * (MAXT - 1) / 2;
 constexpr int NTRI = MAXT * (MAXT - 1) * (MAXT - 2) / 6;
@@ -59,7 +59,9 @@ enum Ctr {
     C_STATIC,                        // static tasks claimed by this device
     C_CONS_REJ,                      // slots rejected by the stack consensus row rule
     C_ROUNDS,                        // enumeration rounds (a round pops up to 16 nodes)
-    C_NCTR
+    C_LVL0,                          // diagnostics (PMS8G_LEVELSTATS builds): per push level k, 6 words:
+                                     // pushes, stopped early, slots, survivors of the cheap rules, kept, blocks with a cheap survivor
+    C_NCTR = C_LVL0 + 48
 };
 
 constexpr int NDON = 32;  // enumeration nodes per donated task
@@ -77,14 +79,22 @@ struct QueueState {
     unsigned long long pad[4];
 };
 
-// Dynamic task slot header; kind 1 slots are followed by the donated nodes.
+// Dynamic task slot: header, NDON nodes (kind 1), then the donor's row table
+// and entries of one level (hand-off, see below).
 struct TaskHeader {
     int32_t anchor;  // anchor index
     int16_t kind;    // 0: branch range [a0, a1) at level k; 1: a0 enumeration nodes of the k-tuple
     int16_t k;
     int32_t a0, a1;
     uint32_t stack[MAXT];
-    uint32_t pad[2];
+    // Level hand-off: the donor copies level `hlevel` (k for kind 0, k - 1
+    // for kind 1) into the slot, so the receiver installs it instead of
+    // replaying the prefix pushes 1..hlevel-1 (a replayed depth-1 push of
+    // (50,21) filters ~9,500 entries; installing copies <= 8,000 words).
+    // hlevel = 0: nothing handed off (level 1 is the shared row table, or the
+    // level is larger than SearchParams::don_cap) - the receiver replays.
+    uint32_t hlevel;
+    uint32_t pad;
 };
 
 // Per-warp shared-memory plan (byte offsets inside the warp's region),
@@ -122,6 +132,7 @@ struct SearchParams {
     const uint32_t* task_order;   // static task permutation (heaviest first), or null
     int don_rounds_mask;          // enumeration rounds between starvation checks - 1 (power of two - 1)
     int don_burst;                // node batches donated per check at most
+    int don_gen_mask;             // generic enumeration loop: rounds between starvation checks - 1 (power of two - 1)
     int lazy;                     // 1: rows of the final level are filtered on demand
     int reorder;   // 1: agreement-first enumeration order (0: natural, exact_tree)
     uint32_t* scratch;            // per-warp level storage + node stack
@@ -143,6 +154,8 @@ struct SearchParams {
     unsigned long long jitter_ns;
     unsigned long long jitter_seed;
     int cons_rows;  // 1: push filters apply the stack consensus bound to every remaining row
+    int don_cap;       // level entries a dynamic task slot can carry (0: no hand-off)
+    int qslot_lvl_off; // byte offset of the handed-off LevelMeta + entries inside a slot
     int claim_chunk;                // shared queue: static tasks per CAS far from the tail
     long long chunk_until;          // ... while more than this many remain
 };

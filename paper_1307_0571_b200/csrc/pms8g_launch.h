@@ -13,7 +13,8 @@ size_t lmer_bytes(int W);
 size_t node_bytes(int W);
 WarpPlan make_plan(int W, int l, int t);
 size_t search_smem(int W, int K, int warps, const WarpPlan& plan);
-size_t task_slot_bytes(int W);
+size_t task_slot_bytes(int W, int don_cap);
+size_t task_slot_level_offset(int W);
 
 cudaError_t launch_encode(int W, const uint8_t* codes, int n, int m, int l, int w, void* table, int* err,
                           cudaStream_t s);

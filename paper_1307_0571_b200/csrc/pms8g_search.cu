@@ -29,11 +29,16 @@ using namespace dev;
 
 namespace {
 
+// push filters of builds with t >= this stop at the first emptied row
+#ifndef PMS8G_EARLYOUT_MT
+#define PMS8G_EARLYOUT_MT 5
+#endif
+
 template <int W>
 struct Node {
     Lmer<W> c;    // candidate prefix planes
     uint32_t rA;  // budgets of members 0..3, biased by +64, one byte each
-    uint32_t rB;  // budgets of members 4..5 (bytes 0,1); prefix length p in byte 3
+    uint32_t rB;  // budgets of members 4..6 (bytes 0..2); prefix length p in byte 3
 };
 
 extern __shared__ __align__(16) uint8_t dyn_smem[];
@@ -575,6 +580,14 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     __syncwarp();
     int out = 0;
     unsigned pair_rej = 0, tri_rej = 0, cons_rej = 0;
+    // early exit on an emptied row (builds where non-viable pushes are common)
+    constexpr bool kEarlyOut = MT >= PMS8G_EARLYOUT_MT;
+#ifdef PMS8G_LEVELSTATS
+    unsigned ls_cheap = 0, ls_blocks = 0;
+#endif
+    unsigned seg_kept = 0u;  // the row segment open at the block start kept an entry
+    int n_done = n_iter;
+    bool dead = false;
     // the next block's entries are loaded one iteration ahead (the level
     // entries stream from L2; this hides one load latency per block)
     auto load_entry = [&](int f) -> uint32_t {
@@ -620,6 +633,10 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 pair_rej += !keep;
             }
         }
+#ifdef PMS8G_LEVELSTATS
+        ls_cheap += keep;
+        ls_blocks += __any_sync(0xffffffffu, keep) ? 1u : 0u;
+#endif
         if constexpr (MT >= 5) {
             // Theorem 1 against the older members: skipped by the whole warp
             // when no lane survived the cheap rules (most blocks at depth;
@@ -641,6 +658,26 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if constexpr (kEarlyOut) {
+            // a row that ends in this block without a survivor makes the push
+            // non-viable: stop (at t >= 5 most pushes end this way). `ends`
+            // marks the last entry of each row segment; a carry chain over the
+            // non-end positions tells per segment whether it kept anything.
+            const uint32_t nxt_blk = __shfl_sync(0xffffffffu, e_next, 0);
+            const uint32_t nxt_lane = __shfl_down_sync(0xffffffffu, e, 1);
+            const uint32_t nxt = lane == 31 ? nxt_blk : nxt_lane;
+            const unsigned ends = __ballot_sync(0xffffffffu, valid && (nxt >> 24) != (e >> 24));
+            const unsigned balc = bal | seg_kept;
+            const unsigned mid = ~ends;
+            const unsigned nonempty = (((balc & mid) + mid) & ends) | (balc & ends);
+            if (ends & ~nonempty) {
+                n_done = min(base + 32, n_iter);
+                dead = true;
+                break;
+            }
+            if (ends) seg_kept = (ends >> 31) ? 0u : ((bal >> (32 - __clz(ends))) != 0u ? 1u : 0u);
+            else seg_kept |= bal != 0u ? 1u : 0u;
+        }
         if (MT < 5 || bal) {  // warp-uniform: deep blocks without survivors write nothing
             if (keep) dst[out + __popc(bal & lanemask_lt())] = e;
             out += __popc(bal);
@@ -656,7 +693,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     // an emptied row is detected after the pass (almost every push is viable,
     // so the pass rarely could have stopped early)
     C.add(W_PUSH, 1);
-    C.add(W_SLOTS, static_cast<unsigned long long>(n_iter));
+    C.add(W_SLOTS, static_cast<unsigned long long>(n_done));
     {
         unsigned pr = pair_rej, tr = tri_rej, cr = cons_rej;
 #pragma unroll
@@ -669,8 +706,24 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         C.add(W_TRIREJ, tr);
         C.add(W_CONSREJ, cr);
     }
-    bool ok = true;
+#ifdef PMS8G_LEVELSTATS
     {
+        unsigned ch = ls_cheap;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) ch += __shfl_xor_sync(0xffffffffu, ch, sh);
+        if (lane == 0) {
+            unsigned long long* q = P.counters + C_LVL0 + 6 * min(k, 7);
+            atomicAdd(q + 0, 1ull);
+            atomicAdd(q + 1, dead ? 1ull : 0ull);
+            atomicAdd(q + 2, static_cast<unsigned long long>(n_done));
+            atomicAdd(q + 3, static_cast<unsigned long long>(ch));
+            atomicAdd(q + 4, static_cast<unsigned long long>(out));
+            atomicAdd(q + 5, static_cast<unsigned long long>(ls_blocks));
+        }
+    }
+#endif
+    bool ok = !dead;
+    if (ok) {
         const int nr2 = nrows - 1;
         int c = 0;
         uint8_t row = 0;
@@ -846,8 +899,14 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
 // 2r+1 once published, and the consumer frees it for round r+1 (2r+2) after
 // copying the task out, so a slot is never overwritten while being read.
 template <int W, int MT, typename F>
-__device__ __noinline__ void publish(WarpCtx<W, MT>& C, const TaskHeader& h, int nnodes, F getnode) {
+__device__ __noinline__ void publish(WarpCtx<W, MT>& C, TaskHeader& h, int nnodes, F getnode) {
     const SearchParams& P = *C.P;
+    // level handed off with the task (TaskHeader::hlevel)
+    {
+        const int hl = h.kind == 0 ? h.k : h.k - 1;
+        h.hlevel = (hl >= 2 && C.S()->lev[hl].total <= P.don_cap) ? static_cast<uint32_t>(hl) : 0u;
+        h.pad = 0;
+    }
     unsigned long long s = 0;
     if (C.lane == 0) {
         s = atomicAdd(&P.qs->alloc, 1ull);
@@ -862,6 +921,17 @@ __device__ __noinline__ void publish(WarpCtx<W, MT>& C, const TaskHeader& h, int
     for (int x = C.lane; x < static_cast<int>(sizeof(TaskHeader) / 4); x += 32) hd[x] = hs[x];
     Node<W>* nd = reinterpret_cast<Node<W>*>(slot + sizeof(TaskHeader));
     for (int x = C.lane; x < nnodes; x += 32) nd[x] = getnode(x);
+    if (h.hlevel) {
+        const LevelMeta& L = C.S()->lev[h.hlevel];
+        uint32_t* lm = reinterpret_cast<uint32_t*>(slot + P.qslot_lvl_off);
+        const uint32_t* ms = reinterpret_cast<const uint32_t*>(&L);
+        constexpr int MW = static_cast<int>(sizeof(LevelMeta) / 4);
+        for (int x = C.lane; x < MW; x += 32) lm[x] = ms[x];
+        const uint32_t* es = level_entries<W, MT>(C, static_cast<int>(h.hlevel));
+        uint32_t* ed = lm + MW;
+        const int tot = L.total;
+        for (int x = C.lane; x < tot; x += 32) ed[x] = es[x];
+    }
     __threadfence();
     __syncwarp();
     if (C.lane == 0) {
@@ -912,7 +982,6 @@ __device__ __noinline__ void maybe_donate_dfs(WarpCtx<W, MT>& C, int kmin, int k
             h.a1 = end;
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) h.stack[i] = i < kk ? S.stack_id[i] : 0u;
-            h.pad[0] = h.pad[1] = 0;
             __syncwarp();
             if (C.lane == 0) S.iter_end[kk] = mid;
             __syncwarp();
@@ -1710,8 +1779,7 @@ __device__ __noinline__ void enum_loop_fast(WarpCtx<1, MT>& C, int t, const Leve
                     h.a1 = 0;
 #pragma unroll
                     for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
-                    h.pad[0] = h.pad[1] = 0;
-                    if (nov >= NDON) {
+                            if (nov >= NDON) {
                         const int o0 = nov - NDON;
                         publish<1, MT>(C, h, NDON, [&](int x) { return C.node_glob[o0 + x]; });
                         nov -= NDON;
@@ -1900,7 +1968,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
             } else {
                 const uint32_t b = static_cast<uint32_t>(P.d + 64);
                 root.rA = b | (b << 8) | (b << 16) | (b << 24);
-                root.rB = b | (b << 8);
+                root.rB = b | (b << 8) | (b << 16);
             }
             ns[0] = root;
         }
@@ -1925,7 +1993,7 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
             __syncwarp();
         }
         // donate the shallowest nodes when other warps are starving
-        if (P.donate && ((++rounds & 7) == 0) && (nov >= NDON || nn >= NDON + 16) && starving<W, MT>(C)) {
+        if (P.donate && ((++rounds & P.don_gen_mask) == 0) && (nov >= NDON || nn >= NDON + 16) && starving<W, MT>(C)) {
             TaskHeader h;
             h.anchor = C.anchor;
             h.kind = 1;
@@ -1935,7 +2003,6 @@ __device__ __noinline__ void enumerate_verify(WarpCtx<W, MT>& C, int t, int ndon
             h.a1 = 0;
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) h.stack[i] = i < t ? S.stack_id[i] : 0u;
-            h.pad[0] = h.pad[1] = 0;
             if (nov >= NDON) {
                 const int o0 = nov - NDON;
                 publish<W, MT>(C, h, NDON, [&](int x) { return ov[o0 + x]; });
@@ -2198,6 +2265,21 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
                 }
             }
             __syncwarp();
+            // install the handed-off level (row table + entries) into this
+            // warp's own level buffer
+            const int hl = static_cast<int>(S.task.hlevel);
+            if (hl >= 2) {
+                const uint32_t* lm = reinterpret_cast<const uint32_t*>(slot + P.qslot_lvl_off);
+                constexpr int MW = static_cast<int>(sizeof(LevelMeta) / 4);
+                uint32_t* md = reinterpret_cast<uint32_t*>(&S.lev[hl]);
+                for (int x = lane; x < MW; x += 32) md[x] = __ldcg(lm + x);
+                __syncwarp();
+                const int tot = S.lev[hl].total;
+                uint32_t* ed = level_entries<W, MT>(C, hl);
+                const uint32_t* es = lm + MW;
+                for (int x = lane; x < tot; x += 32) ed[x] = __ldcg(es + x);
+                __syncwarp();
+            }
             if (lane == 0) {
                 __threadfence();
                 atomicExch(&P.qstate[idx % qcap], 2u * static_cast<unsigned int>(idx / qcap) + 2u);
@@ -2209,9 +2291,10 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             if (lane < MAXT && lane >= 1 && lane < tk) S.stack_id[lane] = S.task.stack[lane];
             __syncwarp();
             if (P.log_cycles) tdiag[1] = clock64() - task_t0;
-            // replay the prefix pushes to rebuild levels 2..tk
+            // replay the prefix pushes to rebuild levels 2..tk (from the
+            // handed-off level on when there is one)
             bool ok = true;
-            for (int i = 1; i < tk && ok; ++i) {
+            for (int i = hl >= 2 ? hl : 1; i < tk && ok; ++i) {
                 ok = (i + 1 == t && P.lazy) ? lazy_push<W, MT>(C, i) : filter_push<W, MT>(C, i);
                 if (P.log_cycles && i == 1) tdiag[2] = clock64() - task_t0;
                 C.add(W_REPLAYS, 1);
@@ -2317,7 +2400,13 @@ size_t search_smem(int W, int K, int warps, const WarpPlan& plan) {
     return (rows * lmer_bytes(W) + 15) / 16 * 16 + static_cast<size_t>(plan.bytes) * warps;
 }
 
-size_t task_slot_bytes(int W) { return (sizeof(TaskHeader) + NDON * node_bytes(W) + 127) / 128 * 128; }
+// slot = header | NDON nodes | (don_cap > 0) LevelMeta + don_cap entries
+size_t task_slot_level_offset(int W) { return (sizeof(TaskHeader) + NDON * node_bytes(W) + 15) / 16 * 16; }
+size_t task_slot_bytes(int W, int don_cap) {
+    size_t b = task_slot_level_offset(W);
+    if (don_cap > 0) b += sizeof(LevelMeta) + sizeof(uint32_t) * static_cast<size_t>(don_cap);
+    return (b + 127) / 128 * 128;
+}
 
 template <int W, int MT>
 cudaError_t set_smem_t(size_t bytes) {
@@ -2350,8 +2439,8 @@ cudaError_t set_search_smem(int W, int t, size_t bytes) {
         if (e == cudaSuccess) cur = bytes;                \
         return e;                                         \
     }
-    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
-    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6)
+    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6) PMS8G_CASE(1, 7)
+    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6) PMS8G_CASE(2, 7)
 #undef PMS8G_CASE
     return cudaErrorInvalidValue;
 }
@@ -2369,8 +2458,8 @@ cudaError_t launch_search(int W, const SearchParams& P, int blocks, int warps, s
         search_kernel<WW, M, 16><<<blocks, warps * 32, smem, s>>>(P);     \
         return cudaGetLastError();                                        \
     }
-    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6)
-    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6)
+    PMS8G_CASE(1, 2) PMS8G_CASE(1, 3) PMS8G_CASE(1, 4) PMS8G_CASE(1, 5) PMS8G_CASE(1, 6) PMS8G_CASE(1, 7)
+    PMS8G_CASE(2, 2) PMS8G_CASE(2, 3) PMS8G_CASE(2, 4) PMS8G_CASE(2, 5) PMS8G_CASE(2, 6) PMS8G_CASE(2, 7)
 #undef PMS8G_CASE
     return cudaErrorInvalidValue;
 }

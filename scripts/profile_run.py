@@ -47,6 +47,15 @@ if len(c) > 55:
               f"nodes={r[6]} prologue_cycles={r[7]}")
     print(f"  idle warp-cycles {c[55]:.3e} busy(filter+pattern) {c[8] + c[9]:.3e}"
           + (f" of {tot:.3e} available: idle {c[55] / tot:.1%}" if tot else ""))
+if len(c) > 395:
+    print(f"  cons_rej={c[395]}")
+if len(c) > 397 + 48 - 1 and any(c[397:445]):
+    for k in range(8):
+        r = c[397 + 6 * k:403 + 6 * k]
+        if r[0]:
+            print(f"  level {k}: pushes={r[0]} stopped_early={r[1]} slots/push={r[2] / r[0]:.0f} "
+                  f"cheap_survivors/push={r[3] / r[0]:.1f} kept/push={r[4] / r[0]:.1f} "
+                  f"blocks_with_survivor/push={r[5] / r[0]:.1f} of {r[2] / r[0] / 32:.1f}")
 if len(c) > 396 and c[396]:
     print(f"  enumeration rounds {c[396]} nodes/round {c[7] / c[396]:.2f} (fast loop, up to 16)")
 print("  task cycles histogram (log2 bucket: count): " +

@@ -140,5 +140,5 @@ def test_gpu_switch_depth_rule():
     # host-side model (no device): the GPU-tuned switch depth of the five
     # BASELINE configs; the reference's own rule gives 2,3,3,3,5
     cfgs = [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]
-    assert [P.gpu_threshold(20, 600, l, d) for l, d in cfgs] == [2, 3, 4, 4, 6]
+    assert [P.gpu_threshold(20, 600, l, d) for l, d in cfgs] == [2, 3, 4, 4, 7]
     assert [P.estimate_threshold(20, 600, l, d) for l, d in cfgs] == [2, 3, 3, 3, 5]

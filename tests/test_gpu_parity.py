@@ -93,14 +93,15 @@ def test_full_instance_21_8_against_every_reference_anchor():
 
 
 @pytest.mark.parametrize("l,d,n,m,seed", [(34, 10, 6, 60, 1), (38, 11, 6, 60, 2), (45, 13, 5, 60, 6),
-                                          (28, 9, 6, 50, 7), (24, 8, 6, 60, 5)])
+                                          (28, 9, 6, 50, 7), (24, 8, 6, 60, 5), (36, 11, 8, 60, 3),
+                                          (26, 8, 9, 50, 4)])
 def test_deep_switch_depths_against_oracle(l, d, n, m, seed):
-    # the t >= 4 builds (consensus row rule, stack bound, 5/6-member tuples) on
+    # the t >= 4 builds (consensus row rule, stack bound, 5/6/7-member tuples) on
     # one- and two-word l-mers, every t against the complete C oracle
     inst = planted(l, d, seed, n=n, m=m)
     want, _ = O.solve(inst.codes, l, d)
     assert inst.motif in want
-    for t in range(3 if l > 32 else 2, min(n, 6) + 1):  # t=2 on l > 32: minutes of enumeration
+    for t in range(3 if l > 32 else 2, min(n, 7) + 1):  # t=2 on l > 32: minutes of enumeration
         assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == want, t
 
 
@@ -301,7 +302,7 @@ def test_anchor_planted_21_8_and_23_9():
 
 def test_gpu_threshold_rule():
     assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
-        [2, 3, 4, 4, 6]
+        [2, 3, 4, 4, 7]
 
 
 @pytest.mark.parametrize("split", ["static", "queue"])
