@@ -1258,7 +1258,9 @@ int run_pipeline(pms8g_ctx* c, char* err, size_t errlen) {
             P.don_cap = c->don_cap;
             P.qslot_lvl_off = static_cast<int>(task_slot_level_offset(c->W));
             P.donate = std::getenv("PMS8G_NO_DONATE") ? 0 : 1;
-            P.don_pushes = 32;  // DFS pushes between starvation checks (4: +1.8 % on (17,6), +1.6 % (21,8))
+            // DFS pushes between starvation checks: 32 for the short pushes of t <= 3 (4: +1.8 % on
+            // (17,6)); t >= 4 pushes are long, 4 feeds the tail sooner ((23,9) 29 S1 l-mers 483 -> 444 ms)
+            P.don_pushes = c->t >= 4 ? 4 : 32;
             P.don_rounds_mask = 63;
             P.don_burst = 1;
             // generic (two-word / t >= 5) enumeration: a check per round measured slower

@@ -29,6 +29,21 @@ using namespace dev;
 
 namespace {
 
+// per-rule rejection counters of the push filters (pair_rej, tri_rej,
+// cons_rej): diagnostics builds only (three adds per slot and 15 shuffles per
+// push otherwise)
+#ifdef PMS8G_LEVELSTATS
+#define PMS8G_REJ(x) (x)
+#else
+#define PMS8G_REJ(x) ((void)0)
+#endif
+
+// push filters of builds with t >= this queue the survivors of the cheap rules
+// and run Theorem 1 on full warps of them (WarpFixed::qe)
+#ifndef PMS8G_QUEUE_MT
+#define PMS8G_QUEUE_MT 5
+#endif
+
 // push filters of builds with t >= this stop at the first emptied row
 #ifndef PMS8G_EARLYOUT_MT
 #define PMS8G_EARLYOUT_MT 5
@@ -84,6 +99,11 @@ struct WarpFixed {
     // consensus row rule: slot k = masks of stack[0..k-1] (cons_prepare);
     // 12-word (16-byte aligned) slots so a filter loads them with LDS.128
     __align__(16) uint32_t cons[MAXT + 1][12];
+    // push filters of the t >= PMS8G_QUEUE_MT builds: survivors of the cheap
+    // rules (consensus, pair) wait here, with their l-mers, until 32 of them
+    // run the Theorem-1 triple rule together (circular, 64 slots)
+    __align__(16) uint32_t qv[64][4];
+    uint32_t qe[64];
 };
 
 
@@ -579,7 +599,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     if (lane == 0) S.lazy_level = 0;
     __syncwarp();
     int out = 0;
-    unsigned pair_rej = 0, tri_rej = 0, cons_rej = 0;
+    [[maybe_unused]] unsigned pair_rej = 0, tri_rej = 0, cons_rej = 0;
     // early exit on an emptied row (builds where non-viable pushes are common)
     constexpr bool kEarlyOut = MT >= PMS8G_EARLYOUT_MT;
 #ifdef PMS8G_LEVELSTATS
@@ -588,6 +608,45 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     unsigned seg_kept = 0u;  // the row segment open at the block start kept an entry
     int n_done = n_iter;
     bool dead = false;
+    // survivors of the cheap rules queue up (WarpFixed::qe/qv); Theorem 1
+    // against the older members runs on 32 of them at a time, and the kept
+    // ones are appended to the new level (flat order is preserved)
+    constexpr bool kQueue = MT >= PMS8G_QUEUE_MT && StackSet<W, MT>::kSmem;
+    int qh = 0, qn = 0;
+    auto resolve = [&](int cntq) {
+        const bool have = lane < cntq;
+        uint32_t qe = 0u;
+        bool kp = false;
+        if (have) {
+            const int qi = (qh + lane) & 63;
+            qe = S.qe[qi];
+            Lmer<W> QV;
+            if constexpr (W == 2) {
+                const uint4 v = *reinterpret_cast<const uint4*>(S.qv[qi]);
+                QV.h[0] = v.x, QV.h[W - 1] = v.y, QV.o[0] = v.z, QV.o[W - 1] = v.w;
+            } else {
+                const uint2 v = *reinterpret_cast<const uint2*>(S.qv[qi]);
+                QV.h[0] = v.x, QV.o[0] = v.y;
+            }
+            const Mask<W> qmu = mism<W>(QV, U);
+            const int qhvu = popcm<W>(qmu);
+            kp = true;
+            for (int i = 0; i < k; ++i)
+                if (kp) kp = ss.triple_ok(i, QV, qmu, qhvu, six_d);
+            PMS8G_REJ(tri_rej += !kp);
+        }
+        const unsigned b2 = __ballot_sync(0xffffffffu, kp);
+        if (b2) {
+            if (kp) dst[out + __popc(b2 & lanemask_lt())] = qe;
+            out += __popc(b2);
+            const uint32_t row = qe >> 24;
+            const unsigned grp = __match_any_sync(0xffffffffu, row) & b2;
+            if (kp && __ffs(grp) - 1 == lane) S.cnt_by_row[row] += static_cast<uint32_t>(__popc(grp));
+        }
+        __syncwarp();
+        qh = (qh + cntq) & 63;
+        qn -= cntq;
+    };
     // the next block's entries are loaded one iteration ahead (the level
     // entries stream from L2; this hides one load latency per block)
     auto load_entry = [&](int f) -> uint32_t {
@@ -624,19 +683,59 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             keep = true;
             if (cons) {
                 keep = cons_pass<W>(cm, V);
-                cons_rej += !keep;
+                PMS8G_REJ(cons_rej += !keep);
             }
             if (keep) {
                 mu = mism<W>(V, U);
                 hvu = popcm<W>(mu);
                 keep = hvu <= two_d;
-                pair_rej += !keep;
+                PMS8G_REJ(pair_rej += !keep);
             }
         }
 #ifdef PMS8G_LEVELSTATS
         ls_cheap += keep;
         ls_blocks += __any_sync(0xffffffffu, keep) ? 1u : 0u;
 #endif
+        if constexpr (kQueue) {
+            const unsigned cb = __ballot_sync(0xffffffffu, keep);
+            if constexpr (kEarlyOut) {
+                // a row that ends in this block without a survivor of the
+                // cheap rules makes the push non-viable: stop (at t >= 5 most
+                // pushes end this way). `ends` marks the last entry of each
+                // row segment; a carry chain over the non-end positions tells
+                // per segment whether it kept anything. (Rows emptied by
+                // Theorem 1 alone are found after the pass.)
+                const uint32_t nxt_blk = __shfl_sync(0xffffffffu, e_next, 0);
+                const uint32_t nxt_lane = __shfl_down_sync(0xffffffffu, e, 1);
+                const uint32_t nxt = lane == 31 ? nxt_blk : nxt_lane;
+                const unsigned ends = __ballot_sync(0xffffffffu, valid && (nxt >> 24) != (e >> 24));
+                const unsigned balc = cb | seg_kept;
+                const unsigned mid = ~ends;
+                const unsigned nonempty = (((balc & mid) + mid) & ends) | (balc & ends);
+                if (ends & ~nonempty) {
+                    n_done = min(base + 32, n_iter);
+                    dead = true;
+                    break;
+                }
+                if (ends) seg_kept = (ends >> 31) ? 0u : ((cb >> (32 - __clz(ends))) != 0u ? 1u : 0u);
+                else seg_kept |= cb != 0u ? 1u : 0u;
+            }
+            if (cb) {
+                if (keep) {
+                    const int qi = (qh + qn + __popc(cb & lanemask_lt())) & 63;
+                    S.qe[qi] = e;
+                    if constexpr (W == 2) {
+                        *reinterpret_cast<uint4*>(S.qv[qi]) = make_uint4(V.h[0], V.h[W - 1], V.o[0], V.o[W - 1]);
+                    } else {
+                        *reinterpret_cast<uint2*>(S.qv[qi]) = make_uint2(V.h[0], V.o[0]);
+                    }
+                }
+                qn += __popc(cb);
+                __syncwarp();
+                if (qn >= 32) resolve(32);
+            }
+            continue;
+        }
         if constexpr (MT >= 5) {
             // Theorem 1 against the older members: skipped by the whole warp
             // when no lane survived the cheap rules (most blocks at depth;
@@ -646,14 +745,14 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 const bool before = keep;
                 for (int i = 0; i < k; ++i)
                     if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
-                tri_rej += before && !keep;
+                PMS8G_REJ(tri_rej += before && !keep);
             }
         } else {
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 if (i < k && keep) {
                     keep = ss.triple_ok(i, V, mu, hvu, six_d);
-                    tri_rej += !keep;
+                    PMS8G_REJ(tri_rej += !keep);
                 }
             }
         }
@@ -689,11 +788,15 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             __syncwarp();
         }
     }
+    if constexpr (kQueue) {
+        if (!dead && qn > 0) resolve(qn);
+    }
     __syncwarp();
     // an emptied row is detected after the pass (almost every push is viable,
     // so the pass rarely could have stopped early)
     C.add(W_PUSH, 1);
     C.add(W_SLOTS, static_cast<unsigned long long>(n_done));
+#ifdef PMS8G_LEVELSTATS
     {
         unsigned pr = pair_rej, tr = tri_rej, cr = cons_rej;
 #pragma unroll
@@ -706,6 +809,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         C.add(W_TRIREJ, tr);
         C.add(W_CONSREJ, cr);
     }
+#endif
 #ifdef PMS8G_LEVELSTATS
     {
         unsigned ch = ls_cheap;
