@@ -316,11 +316,11 @@ __device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
 }
 
 template <int W, int MT>
-__device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k) {
+__device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k, int slot_index) {
     const SearchParams& P = *C.P;
     const WarpFixed& S = *C.S();
     const int l = P.l;
-    uint32_t* slot = cons_slot<W, MT>(C, k);
+    uint32_t* slot = cons_slot<W, MT>(C, slot_index);
     int sum_m = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -340,20 +340,25 @@ __device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k) {
                 if (i < k) {
                     const Lmer<W> x = C.lmer(S.stack_id[i] & ID_MASK);
                     const uint32_t e = ((c & 2) ? x.h[w] : ~x.h[w]) & ((c & 1) ? x.o[w] : ~x.o[w]) & lm;
+                    // (after members 0..i at most i + 1 of them hold c)
 #pragma unroll
-                    for (int j = MT; j >= 1; --j) ge[c][j] |= ge[c][j - 1] & e;
+                    for (int j = MT; j >= 1; --j)
+                        if (j <= i + 1) ge[c][j] |= ge[c][j - 1] & e;
                 }
             }
 #pragma unroll
-            for (int j = 1; j <= MT; ++j) mg[j] |= ge[c][j];
+            for (int j = 1; j <= MT; ++j)
+                if (j <= k) mg[j] |= ge[c][j];
         }
 #pragma unroll
-        for (int j = 1; j <= MT; ++j) sum_m += __popc(mg[j]);
+        for (int j = 1; j <= MT; ++j)
+            if (j <= k) sum_m += __popc(mg[j]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t g = 0u;
 #pragma unroll
-            for (int j = 1; j <= MT; ++j) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
+            for (int j = 1; j <= MT; ++j)
+                if (j <= k) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
             if (C.lane == c * W + w) slot[c * W + w] = g;
         }
     }
@@ -588,8 +593,10 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const bool cons = cons_rows_at<MT>(P, k);
     ConsMasks<W> cm;
     if (cons) {
-        cons_prepare<W, MT>(C, k + 1);
-        cm = load_cons<W, MT>(C, k + 1);
+        // a fixed slot: its address is the warp's base plus a constant (no
+        // register or spill slot for it inside the filter loop)
+        cons_prepare<W, MT>(C, k + 1, 0);
+        cm = ConsMasks<W>{S.cons[0]};  // from the S view already live in the loop
     }
     const int jb = Ls.branch;
     const int bstart = Ls.start[jb], bcnt = Ls.cnt[jb];
@@ -649,8 +656,11 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     };
     // the next block's entries are loaded one iteration ahead (the level
     // entries stream from L2; this hides one load latency per block)
+    const uint32_t un_iter = static_cast<uint32_t>(n_iter), ubstart = static_cast<uint32_t>(bstart),
+                   ubcnt = static_cast<uint32_t>(bcnt);
     auto load_entry = [&](int f) -> uint32_t {
-        return f < n_iter ? src[f < bstart ? f : f + bcnt] : 0xFFFFFFFFu;
+        const uint32_t uf = static_cast<uint32_t>(f);  // 32-bit unsigned index: one IMAD.WIDE.U32
+        return uf < un_iter ? src[uf + (uf < ubstart ? 0u : ubcnt)] : 0xFFFFFFFFu;
     };
     // software pipeline: entries two blocks ahead, their l-mers (table reads,
     // DSMEM for two-word l-mers) one block ahead
@@ -955,7 +965,7 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
     const int jb = Ls.branch;
     const int nr2 = Ls.nrows - 1;
     const long long f0 = clock64();
-    if (cons_rows_at<MT>(*C.P, k)) cons_prepare<W, MT>(C, k + 1);  // for filter_one_row
+    if (cons_rows_at<MT>(*C.P, k)) cons_prepare<W, MT>(C, k + 1, k + 1);  // for filter_one_row
     int c = 0x7FFF;
     if (lane < nr2) {
         const int j = lane < jb ? lane : lane + 1;
@@ -2471,6 +2481,7 @@ constexpr bool has_deep() {
 }
 
 int search_default_warps(int W, int t) { return W == 1 && t <= 3 ? 12 : 16; }
+
 
 template <int W>
 WarpPlan make_plan_t(int l, int t) {

@@ -10,10 +10,10 @@ for c in 17_6 13_4; do timeout 600 python bench.py --config $c > gpurun_out/benc
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_50_21.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:search_kernel -c 1 -o gpurun_out/r02m_search_50_21 -f \
-  python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_50_21.log 2>&1
+  python scripts/profile_run.py 50 21 0 1 10 > gpurun_out/ncu_50_21.log 2>&1  # the bench step's workload (every 10th S1 offset)
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:search_kernel -c 1 -o gpurun_out/r02m_search_21_8_s10 -f \
   python scripts/profile_run.py 21 8 0 1 10 > gpurun_out/ncu_21_8.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:search_kernel -c 1 -o gpurun_out/r02m_search_17_6 -f \
   python scripts/profile_run.py 17 6 0 1 1 > gpurun_out/ncu_17_6.log 2>&1
-for cfg in "21 8 0 1 10" "17 6 0 1 1" "50 21 0 1 50" "23 9 0 1 20"; do timeout 300 python scripts/profile_run.py $cfg > gpurun_out/prof_$(echo $cfg | cut -d' ' -f1-2 | tr ' ' _).txt 2>&1; done
+for cfg in "21 8 0 1 10" "17 6 0 1 1" "50 21 0 1 10" "23 9 0 1 20" "50 21 0 1 1"; do timeout 300 python scripts/profile_run.py $cfg > gpurun_out/prof_$(echo $cfg | cut -d' ' -f1-2 | tr ' ' _).txt 2>&1; done
 echo done
