@@ -317,52 +317,52 @@ __device__ __forceinline__ uint32_t* cons_slot(const WarpCtx<W, MT>& C, int k) {
 
 template <int W, int MT>
 __device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k, int slot_index) {
+    // Lane c*W + w owns symbol c in word w (the slot's own index): it folds
+    // the k members into ge[j] = positions where at least j of them hold c;
+    // the column maxima come from an OR over the four symbol lanes of a word.
     const SearchParams& P = *C.P;
     const WarpFixed& S = *C.S();
-    const int l = P.l;
+    const int l = P.l, lane = C.lane;
     uint32_t* slot = cons_slot<W, MT>(C, slot_index);
-    int sum_m = 0;
+    const int w = lane % W, c = lane / W;
+    const int nb = min(32, l - 32 * w);
+    uint32_t lm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
+    if (lane >= 4 * W) lm = 0u;  // idle lanes carry zeros through the exchanges
+    const uint32_t fh = (c & 2) ? 0u : 0xffffffffu, fo = (c & 1) ? 0u : 0xffffffffu;
+    uint32_t ge[MT + 1];
+    ge[0] = lm;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const int nb = min(32, l - 32 * w);
-        const uint32_t lm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
-        uint32_t ge[4][MT + 1];  // ge[c][j]: at least j members hold c (j <= k)
-        uint32_t mg[MT + 1];
+    for (int j = 1; j <= MT; ++j) ge[j] = 0u;
 #pragma unroll
-        for (int j = 0; j <= MT; ++j) mg[j] = 0u;
+    for (int i = 0; i < MT; ++i) {
+        if (i < k) {
+            const Lmer<W> x = C.lmer(S.stack_id[i] & ID_MASK);  // one address per warp: a broadcast
+            const uint32_t hw = (W == 2 && w) ? x.h[W - 1] : x.h[0];
+            const uint32_t ow = (W == 2 && w) ? x.o[W - 1] : x.o[0];
+            const uint32_t e = (hw ^ fh) & (ow ^ fo) & lm;  // positions where member i holds c
+            // (after members 0..i at most i + 1 of them hold c)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            ge[c][0] = lm;
-#pragma unroll
-            for (int j = 1; j <= MT; ++j) ge[c][j] = 0u;
-#pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                if (i < k) {
-                    const Lmer<W> x = C.lmer(S.stack_id[i] & ID_MASK);
-                    const uint32_t e = ((c & 2) ? x.h[w] : ~x.h[w]) & ((c & 1) ? x.o[w] : ~x.o[w]) & lm;
-                    // (after members 0..i at most i + 1 of them hold c)
-#pragma unroll
-                    for (int j = MT; j >= 1; --j)
-                        if (j <= i + 1) ge[c][j] |= ge[c][j - 1] & e;
-                }
-            }
-#pragma unroll
-            for (int j = 1; j <= MT; ++j)
-                if (j <= k) mg[j] |= ge[c][j];
-        }
-#pragma unroll
-        for (int j = 1; j <= MT; ++j)
-            if (j <= k) sum_m += __popc(mg[j]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t g = 0u;
-#pragma unroll
-            for (int j = 1; j <= MT; ++j)
-                if (j <= k) g |= mg[j] & (j < MT ? ~mg[j + 1] : 0xffffffffu) & ge[c][j];
-            if (C.lane == c * W + w) slot[c * W + w] = g;
+            for (int j = MT; j >= 1; --j)
+                if (j <= i + 1) ge[j] |= ge[j - 1] & e;
         }
     }
-    if (C.lane == 4 * W) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - sum_m);
+    uint32_t g = 0u, mg_above = 0u;
+    int sum_m = 0;
+#pragma unroll
+    for (int j = MT; j >= 1; --j) {
+        if (j <= k) {  // warp-uniform
+            uint32_t mg = ge[j];  // -> positions whose column maximum is >= j
+            mg |= __shfl_xor_sync(0xffffffffu, mg, W);
+            mg |= __shfl_xor_sync(0xffffffffu, mg, 2 * W);
+            sum_m += __popc(mg);
+            g |= mg & ~mg_above & ge[j];  // maximum == j and c reaches it
+            mg_above = mg;
+        }
+    }
+    if (lane < 4 * W) slot[lane] = g;
+    int tot = __shfl_sync(0xffffffffu, sum_m, 0);
+    if constexpr (W == 2) tot += __shfl_sync(0xffffffffu, sum_m, 1);
+    if (lane == 0) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - tot);
     __syncwarp();
 }
 
@@ -587,7 +587,30 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     const long long f0 = clock64();
 
     const TableRef<W> tr = table_ref<W, MT>(C);
+    const int jb = Ls.branch;
+    const int bstart = Ls.start[jb], bcnt = Ls.cnt[jb];
+    const int n_iter = Ls.total - bcnt;
+    const int nrows = Ls.nrows;
+    // the next block's entries are loaded one iteration ahead (the level
+    // entries stream from L2; this hides one load latency per block)
+    const uint32_t un_iter = static_cast<uint32_t>(n_iter), ubstart = static_cast<uint32_t>(bstart),
+                   ubcnt = static_cast<uint32_t>(bcnt);
+    auto load_entry = [&](int f) -> uint32_t {
+        const uint32_t uf = static_cast<uint32_t>(f);  // 32-bit unsigned index: one IMAD.WIDE.U32
+        return uf < un_iter ? src[uf + (uf < ubstart ? 0u : ubcnt)] : 0xFFFFFFFFu;
+    };
+    // software pipeline: entries two blocks ahead, their l-mers (table reads)
+    // one block ahead (t >= 4 builds; the t <= 3 builds keep the one-block
+    // entry prefetch: their register budget goes to the enumeration and
+    // verification loops). The first loads are issued before the per-push
+    // set-up below (stack members, consensus masks), so their latency
+    // overlaps it: most pushes at depth scan only a few blocks.
+    constexpr bool kPipeV = MT >= 4;
+    uint32_t e_next = load_entry(lane);
+    uint32_t e_next2 = kPipeV ? load_entry(lane + 32) : 0u;
     const Lmer<W> U = tr.get(S.stack_id[k] & ID_MASK);
+    Lmer<W> V_next;
+    if constexpr (kPipeV) V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
     StackSet<W, MT> ss;
     ss.load(C, k, U);
     const bool cons = cons_rows_at<MT>(P, k);
@@ -598,10 +621,6 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         cons_prepare<W, MT>(C, k + 1, 0);
         cm = ConsMasks<W>{S.cons[0]};  // from the S view already live in the loop
     }
-    const int jb = Ls.branch;
-    const int bstart = Ls.start[jb], bcnt = Ls.cnt[jb];
-    const int n_iter = Ls.total - bcnt;
-    const int nrows = Ls.nrows;
     if (lane < MAXN) S.cnt_by_row[lane] = 0;
     if (lane == 0) S.lazy_level = 0;
     __syncwarp();
@@ -654,23 +673,6 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         qh = (qh + cntq) & 63;
         qn -= cntq;
     };
-    // the next block's entries are loaded one iteration ahead (the level
-    // entries stream from L2; this hides one load latency per block)
-    const uint32_t un_iter = static_cast<uint32_t>(n_iter), ubstart = static_cast<uint32_t>(bstart),
-                   ubcnt = static_cast<uint32_t>(bcnt);
-    auto load_entry = [&](int f) -> uint32_t {
-        const uint32_t uf = static_cast<uint32_t>(f);  // 32-bit unsigned index: one IMAD.WIDE.U32
-        return uf < un_iter ? src[uf + (uf < ubstart ? 0u : ubcnt)] : 0xFFFFFFFFu;
-    };
-    // software pipeline: entries two blocks ahead, their l-mers (table reads,
-    // DSMEM for two-word l-mers) one block ahead
-    // (t >= 4 builds; the t <= 3 builds keep the one-block entry prefetch:
-    // their register budget goes to the enumeration and verification loops)
-    constexpr bool kPipeV = MT >= 4;
-    uint32_t e_next = load_entry(lane);
-    uint32_t e_next2 = kPipeV ? load_entry(lane + 32) : 0u;
-    Lmer<W> V_next;
-    if constexpr (kPipeV) V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
     for (int base = 0; base < n_iter; base += 32) {
         const int f = base + lane;
         const bool valid = f < n_iter;
