@@ -107,6 +107,29 @@ struct WarpFixed {
 };
 
 
+// Member cache (t >= 4 builds): S.fsm[i] holds the l-mer of stack[i] while it
+// is on the stack - written when the member is set (begin_anchor, a received
+// task's prefix) or first pushed (StackSet::load, lazy_push), so the per-push
+// set-up reads the older members from shared memory instead of the table.
+template <int W>
+__device__ __forceinline__ void cache_member(WarpFixed& S, int i, const Lmer<W>& x) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        S.fsm[i][2 * w] = x.h[w];
+        S.fsm[i][2 * w + 1] = x.o[w];
+    }
+}
+template <int W>
+__device__ __forceinline__ Lmer<W> cached_member(const WarpFixed& S, int i) {
+    Lmer<W> x;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        x.h[w] = S.fsm[i][2 * w];
+        x.o[w] = S.fsm[i][2 * w + 1];
+    }
+    return x;
+}
+
 constexpr int MAXCH = 5;  // candidate chunks of 32 held in registers by verify
 
 // Read-only table load through the non-coherent L1 path (global tables).
@@ -336,7 +359,7 @@ __device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k, int slot_ind
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         if (i < k) {
-            const Lmer<W> x = C.lmer(S.stack_id[i] & ID_MASK);  // one address per warp: a broadcast
+            const Lmer<W> x = cached_member<W>(S, i);  // member cache: a broadcast LDS
             const uint32_t hw = (W == 2 && w) ? x.h[W - 1] : x.h[0];
             const uint32_t ow = (W == 2 && w) ? x.o[W - 1] : x.o[0];
             const uint32_t e = (hw ^ fh) & (ow ^ fo) & lm;  // positions where member i holds c
@@ -522,15 +545,13 @@ struct StackSet {
         S = Sw;
         if constexpr (kSmem) {
             if (C.lane < k) {
-                const Lmer<W> x = tr.get(Sw->stack_id[C.lane] & ID_MASK);
+                const Lmer<W> x = cached_member<W>(*Sw, C.lane);
                 const Mask<W> m = mism<W>(x, U);
 #pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    Sw->fsm[C.lane][2 * w] = x.h[w];
-                    Sw->fsm[C.lane][2 * w + 1] = x.o[w];
-                    Sw->fmiu[C.lane][w] = m.w[w];
-                }
+                for (int w = 0; w < W; ++w) Sw->fmiu[C.lane][w] = m.w[w];
                 Sw->fhs[C.lane] = popcm<W>(m);
+            } else if (C.lane == k) {
+                cache_member<W>(*Sw, k, U);  // the new top joins the member cache
             }
             __syncwarp();
         } else {
@@ -967,7 +988,11 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
     const int jb = Ls.branch;
     const int nr2 = Ls.nrows - 1;
     const long long f0 = clock64();
-    if (cons_rows_at<MT>(*C.P, k)) cons_prepare<W, MT>(C, k + 1, k + 1);  // for filter_one_row
+    if (cons_rows_at<MT>(*C.P, k)) {
+        if (lane == 0) cache_member<W>(S, k, C.lmer(S.stack_id[k] & ID_MASK));
+        __syncwarp();
+        cons_prepare<W, MT>(C, k + 1, k + 1);  // for filter_one_row
+    }
     int c = 0x7FFF;
     if (lane < nr2) {
         const int j = lane < jb ? lane : lane + 1;
@@ -2250,7 +2275,11 @@ __device__ void begin_anchor(WarpCtx<W, MT>& C, int ai) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(P.l1_meta + ai);
     uint32_t* dstm = reinterpret_cast<uint32_t*>(&S.lev[1]);
     for (int x = C.lane; x < static_cast<int>(sizeof(LevelMeta) / 4); x += 32) dstm[x] = src[x];
-    if (C.lane == 0) S.stack_id[0] = static_cast<uint32_t>(P.anchor_off[ai]);
+    if (C.lane == 0) {
+        const uint32_t a = static_cast<uint32_t>(P.anchor_off[ai]);
+        S.stack_id[0] = a;
+        if constexpr (MT >= 4) cache_member<W>(S, 0, C.lmer(a & ID_MASK));
+    }
     __syncwarp();
 }
 
@@ -2404,7 +2433,10 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
             long long tdiag[3] = {0, 0, 0};
             if (P.log_cycles) tdiag[0] = clock64() - task_t0;
             begin_anchor<W, MT>(C, S.task.anchor);
-            if (lane < MAXT && lane >= 1 && lane < tk) S.stack_id[lane] = S.task.stack[lane];
+            if (lane < MAXT && lane >= 1 && lane < tk) {
+                S.stack_id[lane] = S.task.stack[lane];
+                if constexpr (MT >= 4) cache_member<W>(S, lane, C.lmer(S.task.stack[lane] & ID_MASK));
+            }
             __syncwarp();
             if (P.log_cycles) tdiag[1] = clock64() - task_t0;
             // replay the prefix pushes to rebuild levels 2..tk (from the
