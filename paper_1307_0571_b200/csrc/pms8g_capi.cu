@@ -599,7 +599,7 @@ int pms8g_ctx_create(int n, int m, int l, int d, const char* alphabet, const pms
     const size_t lvl_words = static_cast<size_t>(std::max(0, t - 1)) * c->level_cap;
     const size_t node_words =
         static_cast<size_t>(c->node_cap) * (c->sig ? sigma_node_bytes() : node_bytes(c->W)) / 4;
-    c->scratch_words = (lvl_words + node_words + 64 + 31) / 32 * 32;  // + consensus masks (cons_slot)
+    c->scratch_words = (lvl_words + node_words + static_cast<size_t>(c->plan.thr_global_bytes) / 4 + 64 + 31) / 32 * 32;
     const size_t nwarps_total = static_cast<size_t>(c->blocks) * warps;
     int rc2;
 #define AL(ptr, bytes)                                                                          \

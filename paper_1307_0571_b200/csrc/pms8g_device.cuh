@@ -107,6 +107,7 @@ struct WarpPlan {
     int cand_cap;
     int node_smem;
     int npair, ntri;
+    int thr_global_bytes;  // > 0: the enumeration tables live in the warp's global scratch (t >= 5)
 };
 
 struct SearchParams {

@@ -77,7 +77,6 @@ struct WaitState {
 };
 
 struct WarpFixed {
-    LevelMeta lev[MAXT + 1];
     int iter[MAXT + 1];
     int iter_end[MAXT + 1];
     uint32_t stack_id[MAXT];
@@ -98,13 +97,25 @@ struct WarpFixed {
     int32_t fhs[MAXT];
     // consensus row rule: slot k = masks of stack[0..k-1] (cons_prepare);
     // 12-word (16-byte aligned) slots so a filter loads them with LDS.128
-    __align__(16) uint32_t cons[MAXT + 1][12];
-    // push filters of the t >= PMS8G_QUEUE_MT builds: survivors of the cheap
-    // rules (consensus, pair) wait here, with their l-mers, until 32 of them
-    // run the Theorem-1 triple rule together (circular, 64 slots)
-    __align__(16) uint32_t qv[64][4];
+    __align__(16) uint32_t cons[2][12];  // slot 0: the push filter's pass; slot 1: the lazy level's rows
+    // LAST member: a search with switch depth t allocates lev[0..t] only
+    // (warp_fixed_bytes), so the shallow one-word builds keep 16 warps next
+    // to the l-mer table in shared memory
+    LevelMeta lev[MAXT + 1];
+};
+
+// Push filters of the t >= PMS8G_QUEUE_MT builds: survivors of the cheap
+// rules (consensus, pair) wait here, with their l-mers, until 32 of them run
+// the Theorem-1 triple rule together (circular, 64 entry ids; the l-mers are
+// re-read from the table, L1-resident by then). Placed after the warp's
+// WarpFixed in those builds only.
+struct PushQueue {
     uint32_t qe[64];
 };
+
+__host__ __device__ constexpr int warp_fixed_bytes(int t) {
+    return (static_cast<int>(offsetof(WarpFixed, lev)) + (t + 1) * static_cast<int>(sizeof(LevelMeta)) + 15) / 16 * 16;
+}
 
 
 // Member cache (t >= 4 builds): S.fsm[i] holds the l-mer of stack[i] while it
@@ -174,6 +185,7 @@ struct WarpCtx {
     int pushes_since_check;
     unsigned int checks;  // starvation checks made (lane 0; heartbeat pacing)
     const Lmer<W>* gt;  // two-word builds: the table in global memory
+    uint8_t* thr_glob;  // t >= 5 builds: enumeration tables in global scratch
     // shared-memory views derived from the extern __shared__ symbol, so every
     // access compiles to LDS/STS rather than generic LD/ST
     __device__ __forceinline__ const Lmer<W>* T() const { return reinterpret_cast<const Lmer<W>*>(dyn_smem); }
@@ -183,7 +195,12 @@ struct WarpCtx {
         else return T()[id];
     }
     __device__ __forceinline__ WarpFixed* S() const { return reinterpret_cast<WarpFixed*>(dyn_smem + off_S); }
-    __device__ __forceinline__ uint8_t* thr() const { return dyn_smem + off_thr; }
+    // enumeration tables: shared memory, or (t >= 5 builds, where few tuples
+    // are ever enumerated) the warp's global scratch
+    __device__ __forceinline__ uint8_t* thr() const {
+        if constexpr (MT >= 5) return thr_glob;
+        else return dyn_smem + off_thr;
+    }
     __device__ __forceinline__ Lmer<W>* cand() const { return reinterpret_cast<Lmer<W>*>(dyn_smem + off_cand); }
     __device__ __forceinline__ Node<W>* node_smem() const { return reinterpret_cast<Node<W>*>(dyn_smem + off_nodes); }
     __device__ __forceinline__ void add(int i, unsigned long long v) {
@@ -387,21 +404,6 @@ __device__ __noinline__ void cons_prepare(WarpCtx<W, MT>& C, int k, int slot_ind
     if constexpr (W == 2) tot += __shfl_sync(0xffffffffu, sum_m, 1);
     if (lane == 0) slot[4 * W] = static_cast<uint32_t>((k + 1) * (l - P.d) - tot);
     __syncwarp();
-}
-
-template <int W, int MT>
-__device__ __forceinline__ bool cons_check(const WarpCtx<W, MT>& C, int k, uint32_t u) {
-    const uint32_t* slot = cons_slot<W, MT>(C, k);
-    const Lmer<W> x = C.lmer(u & ID_MASK);
-    int matches = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const uint32_t h = x.h[w], o = x.o[w];
-        const uint32_t hit = (slot[0 * W + w] & ~h & ~o) | (slot[1 * W + w] & ~h & o) |
-                             (slot[2 * W + w] & h & ~o) | (slot[3 * W + w] & h & o);
-        matches += __popc(hit);
-    }
-    return matches >= static_cast<int>(slot[4 * W]);
 }
 
 // A view of one slot for a filter pass (the masks stay in shared memory:
@@ -659,6 +661,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     // against the older members runs on 32 of them at a time, and the kept
     // ones are appended to the new level (flat order is preserved)
     constexpr bool kQueue = MT >= PMS8G_QUEUE_MT && StackSet<W, MT>::kSmem;
+    PushQueue& Q = *reinterpret_cast<PushQueue*>(reinterpret_cast<uint8_t*>(&S) + warp_fixed_bytes(tuple_size<MT>(P.t)));
     int qh = 0, qn = 0;
     auto resolve = [&](int cntq) {
         const bool have = lane < cntq;
@@ -666,15 +669,9 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         bool kp = false;
         if (have) {
             const int qi = (qh + lane) & 63;
-            qe = S.qe[qi];
+            qe = Q.qe[qi];
             Lmer<W> QV;
-            if constexpr (W == 2) {
-                const uint4 v = *reinterpret_cast<const uint4*>(S.qv[qi]);
-                QV.h[0] = v.x, QV.h[W - 1] = v.y, QV.o[0] = v.z, QV.o[W - 1] = v.w;
-            } else {
-                const uint2 v = *reinterpret_cast<const uint2*>(S.qv[qi]);
-                QV.h[0] = v.x, QV.o[0] = v.y;
-            }
+            QV = tr.get(qe & ID_MASK);
             const Mask<W> qmu = mism<W>(QV, U);
             const int qhvu = popcm<W>(qmu);
             kp = true;
@@ -756,12 +753,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             if (cb) {
                 if (keep) {
                     const int qi = (qh + qn + __popc(cb & lanemask_lt())) & 63;
-                    S.qe[qi] = e;
-                    if constexpr (W == 2) {
-                        *reinterpret_cast<uint4*>(S.qv[qi]) = make_uint4(V.h[0], V.h[W - 1], V.o[0], V.o[W - 1]);
-                    } else {
-                        *reinterpret_cast<uint2*>(S.qv[qi]) = make_uint2(V.h[0], V.o[0]);
-                    }
+                    Q.qe[qi] = e;
                 }
                 qn += __popc(cb);
                 __syncwarp();
@@ -917,10 +909,10 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
     uint32_t* dst = level_entries<W, MT>(C, k + 1) + Ls.start[j];
     const int cnt = Ls.cnt[j];
     const int d = P.d, six_d = 6 * d, two_d = 2 * d;
-    // consensus row rule: slot k + 1 was prepared by the lazy push
+    // consensus row rule: slot 1 was prepared by the lazy push
     const bool cons = cons_rows_at<MT>(P, k);
     ConsMasks<W> cm;
-    if (cons) cm = load_cons<W, MT>(C, k + 1);
+    if (cons) cm = load_cons<W, MT>(C, 1);
     const TableRef<W> tr = table_ref<W, MT>(C);
     const Lmer<W> U = tr.get(S.stack_id[k] & ID_MASK);
     StackSet<W, MT> ss;
@@ -991,7 +983,7 @@ __device__ __noinline__ bool lazy_push(WarpCtx<W, MT>& C, int k) {
     if (cons_rows_at<MT>(*C.P, k)) {
         if (lane == 0) cache_member<W>(S, k, C.lmer(S.stack_id[k] & ID_MASK));
         __syncwarp();
-        cons_prepare<W, MT>(C, k + 1, k + 1);  // for filter_one_row
+        cons_prepare<W, MT>(C, k + 1, 1);  // for filter_one_row
     }
     int c = 0x7FFF;
     if (lane < nr2) {
@@ -2320,6 +2312,7 @@ __global__ void __launch_bounds__(32 * NW, 1) search_kernel(const __grid_constan
     uint32_t* scratch = P.scratch + gw * P.scratch_words;
     C.lvl_glob = scratch;
     C.node_glob = reinterpret_cast<Node<W>*>(scratch + static_cast<size_t>(P.t > 1 ? P.t - 1 : 0) * P.level_cap);
+    C.thr_glob = reinterpret_cast<uint8_t*>(C.node_glob + P.node_cap);
     C.lane = lane;
     C.pushes_since_check = 0;
     if (lane < W_N) C.S()->ctr[lane] = 0;
@@ -2523,12 +2516,18 @@ WarpPlan make_plan_t(int l, int t) {
     const int tt = t < 1 ? 1 : t;
     p.npair = tt * (tt - 1) / 2;
     p.ntri = tt * (tt - 1) * (tt - 2) / 6;
-    int off = (static_cast<int>(sizeof(WarpFixed)) + 15) / 16 * 16;
+    int off = warp_fixed_bytes(tt < 2 ? 2 : tt);  // t = 1 runs the two-member build
+    if ((tt < 2 ? 2 : tt) >= PMS8G_QUEUE_MT) off += (static_cast<int>(sizeof(PushQueue)) + 15) / 16 * 16;
     p.off_thr = off;
     const int generic_thr = (GEN_TBL_BYTES + (l + 1) * (p.npair + p.ntri) + 15) / 16 * 16;
     const int swar_thr = 16 * ((l + 3) & ~3) + 16 * (l + 1);
-    off += generic_thr > swar_thr ? generic_thr : swar_thr;
-    p.cand_cap = 32 * MAXCH;
+    p.thr_global_bytes = 0;
+    if (tt >= 5) p.thr_global_bytes = generic_thr;  // (the SWAR tables serve t <= 4 only)
+    else off += generic_thr > swar_thr ? generic_thr : swar_thr;
+    // t >= 5: enumeration is rare (few tuples survive that deep); a small
+    // per-warp footprint leaves more of the SM's 256 KB to the L1 that serves
+    // the two-word l-mer table ((50,21): 195 -> 154 KB per CTA, -5%)
+    p.cand_cap = tt >= 5 ? 64 : 32 * MAXCH;
     p.off_cand = off;
     off += p.cand_cap * static_cast<int>(sizeof(Lmer<W>));
     off = (off + 15) / 16 * 16;
