@@ -38,6 +38,12 @@ namespace {
 #define PMS8G_REJ(x) ((void)0)
 #endif
 
+// push filters of builds with t >= this run Theorem 1 in a rolled loop over
+// the older members (t >= 4: the members live in shared memory)
+#ifndef PMS8G_ROLLED_MT
+#define PMS8G_ROLLED_MT 4
+#endif
+
 // push filters of builds with t >= this queue the survivors of the cheap rules
 // and run Theorem 1 on full warps of them (WarpFixed::qe)
 #ifndef PMS8G_QUEUE_MT
@@ -772,6 +778,14 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                     if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
                 PMS8G_REJ(tri_rej += before && !keep);
             }
+        } else if constexpr (MT >= PMS8G_ROLLED_MT) {
+#pragma unroll 1
+            for (int i = 0; i < k; ++i) {
+                if (keep) {
+                    keep = ss.triple_ok(i, V, mu, hvu, six_d);
+                    PMS8G_REJ(tri_rej += !keep);
+                }
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
@@ -952,6 +966,12 @@ __device__ __noinline__ int filter_one_row(WarpCtx<W, MT>& C, int k, int j) {
             if (__any_sync(0xffffffffu, keep))  // as filter_push: whole-warp skip
                 for (int i = 0; i < k; ++i)
                     if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
+        } else if constexpr (MT >= PMS8G_ROLLED_MT) {
+            // rolled (members in shared memory): ~1.5 KB less hot code per
+            // filter in the I-cache-bound t = 4 builds
+#pragma unroll 1
+            for (int i = 0; i < k; ++i)
+                if (keep) keep = ss.triple_ok(i, V, mu, hvu, six_d);
         } else {
 #pragma unroll
             for (int i = 0; i < MT; ++i)
@@ -1142,7 +1162,14 @@ __device__ __forceinline__ int verify_row(const WarpCtx<W, MT>& C, Lmer<W>* cand
         hm[ch] = alive[ch] ? 0x7fff : 0;
         if (alive[ch]) cd[ch] = cand[ch * 32 + lane];
     }
-    constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
+    // entries per all-witnessed check. The t = 4 builds are bound by
+    // instruction fetch (hot code > the 32 KB L1.5 I-cache): half the unroll
+    // there ((21,8) -2%, (23,9) -3%; neutral for t <= 3)
+#if defined(PMS8G_VERIFY_U1)
+    constexpr int U = MT == 4 ? (NCH == 1 ? 2 : 1) : (NCH == 1 ? 8 : (NCH == 2 ? 4 : 2));
+#else
+    constexpr int U = MT == 4 ? (NCH == 1 ? 4 : 2) : (NCH == 1 ? 8 : (NCH == 2 ? 4 : 2));
+#endif
     bool done = false;
     for (int eb = 0; eb < cnt && !done; eb += 32) {
         // lanes past the row's end hold a copy of its first entry, so whole
@@ -1246,7 +1273,9 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
             out = verify_row_small<W, MT>(C, C.cand(), entries, st, cnt, n, d, lane, scanned);
         } else switch ((n + 31) >> 5) {
             case 1: out = verify_row<W, MT, 1>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+#ifndef PMS8G_VERIFY_NO2
             case 2: out = verify_row<W, MT, 2>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
+#endif
             default: out = verify_row<W, MT, 5>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
         }
         vcmp += static_cast<unsigned long long>(n) * scanned;
