@@ -17,6 +17,7 @@
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <functional>
 #include <mutex>
 #include <random>
 #include <string>
@@ -819,6 +820,59 @@ bool same_shape(const pms8g_ctx* c, int n, int m, int l, int d, const char* alph
 }
 }  // namespace
 
+}  // extern "C" (reopened below)
+
+namespace pms8g {
+// More than MAXN sequences (the reference takes any n, src/problem.cpp:7-28):
+// a motif of all n sequences is a motif of the first MAXN, and the search is
+// exact, so the motif set of the first MAXN sequences contains the answer;
+// the GPU scanner (naive_is_motif over every sequence) keeps exactly the
+// members that also occur in the remaining ones. The warp's row tables stay
+// lane-indexed (32 rows). `solve_head` searches the first MAXN sequences.
+int solve_many_sequences(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet,
+                         const pms8g_options& opt, pms8g_result* out, char* err, size_t errlen,
+                         const std::function<int(const pms8g_options&, pms8g_result*)>& solve_head) {
+    const int sig = alphabet ? static_cast<int>(std::strlen(alphabet)) : 4;
+    if (sig > 4)
+        return fail(err, errlen, PMS8G_ERR_INVALID,
+                    "GPU path supports n <= %d sequences for alphabets above 4 symbols, got %d", MAXN, n);
+    if (opt.branches)
+        return fail(err, errlen, PMS8G_ERR_INVALID, "branch subsets need n <= %d sequences, got %d", MAXN, n);
+    pms8g_options sub_opt = opt;
+    sub_opt.max_motifs = -1;  // the cap applies to the instance's own motifs, below
+    pms8g_result sub;
+    int rc = solve_head(sub_opt, &sub);
+    if (rc) return rc;
+    const char* alpha = alphabet ? alphabet : "ACGT";
+    const int64_t cnt = sub.count;
+    std::vector<uint8_t> mc(static_cast<size_t>(cnt) * l), pass(static_cast<size_t>(cnt));
+    std::vector<int32_t> wit(static_cast<size_t>(cnt) * n);
+    for (int64_t i = 0; i < cnt * l; ++i) mc[i] = static_cast<uint8_t>(std::strchr(alpha, sub.motifs[i]) - alpha);
+    rc = pms8g_verify_motifs(codes, n, m, l, d, alphabet, mc.data(), cnt, wit.data(), pass.data(), opt.device, err,
+                             errlen);
+    if (rc) {
+        pms8g_result_free(&sub);
+        return rc;
+    }
+    int64_t kept = 0;
+    for (int64_t i = 0; i < cnt; ++i)
+        if (pass[i]) {
+            if (kept != i) std::memmove(sub.motifs + kept * l, sub.motifs + i * l, static_cast<size_t>(l));
+            ++kept;
+        }
+    sub.motifs[kept * l] = 0;
+    sub.count = kept;
+    if (opt.max_motifs >= 0 && kept > opt.max_motifs) {
+        pms8g_result_free(&sub);
+        return fail(err, errlen, PMS8G_ERR_RUNTIME, "motif cap of %lld exceeded", static_cast<long long>(opt.max_motifs));
+    }
+    *out = sub;
+    return PMS8G_OK;
+}
+}  // namespace pms8g
+
+extern "C" {
+
 int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet, const pms8g_options* opt_in,
                 pms8g_result* out, char* err, size_t errlen) {
     const double t0 = now_s();
@@ -826,6 +880,14 @@ int pms8g_solve(const uint8_t* codes, int n, int m, int l, int d, const char* al
     pms8g_options opt;
     if (opt_in) opt = *opt_in;
     else pms8g_default_options(&opt);
+    if (n > MAXN) {
+        const int rc = solve_many_sequences(codes, n, m, l, d, alphabet, opt, out, err, errlen,
+                                            [&](const pms8g_options& o, pms8g_result* r) {
+                                                return pms8g_solve(codes, MAXN, m, l, d, alphabet, &o, r, err, errlen);
+                                            });
+        if (!rc) out->report.wall_seconds = now_s() - t0;
+        return rc;
+    }
     int sigma = 0;
     int rc = validate_problem(n, m, l, d, alphabet, err, errlen, &sigma);
     if (rc) return rc;

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
+#include <functional>
 
 #include "../../include/pms8g.h"
 
@@ -44,6 +45,12 @@ struct MergeScratch {
 int merge_keys_with(MergeScratch& m, const void* dev_in, long long count, void* dev_out, long long* out_count,
                     cudaStream_t stream, char* err, size_t errlen);
 void merge_scratch_free(MergeScratch& m);
+
+// n > 32 sequences: search the first 32 (solve_head), keep the motifs the GPU
+// scanner confirms in all n (pms8g_capi.cu).
+int solve_many_sequences(const uint8_t* codes, int n, int m, int l, int d, const char* alphabet,
+                         const pms8g_options& opt, pms8g_result* out, char* err, size_t errlen,
+                         const std::function<int(const pms8g_options&, pms8g_result*)>& solve_head);
 
 }  // namespace pms8g
 

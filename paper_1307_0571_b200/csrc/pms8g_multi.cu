@@ -388,6 +388,12 @@ int pms8g_solve_multi(const uint8_t* codes, int n, int m, int l, int d, const ch
     pms8g_options opt;
     if (opt_in) opt = *opt_in;
     else pms8g_default_options(&opt);
+    if (n > 32)  // MAXN: search the first 32 sequences on the GPUs, scan the rest (pms8g_capi.cu)
+        return solve_many_sequences(codes, n, m, l, d, alphabet, opt, out, err, errlen,
+                                    [&](const pms8g_options& o, pms8g_result* r) {
+                                        return pms8g_solve_multi(codes, 32, m, l, d, alphabet, &o, devices,
+                                                                 ndevices, r, err, errlen);
+                                    });
     std::lock_guard<std::mutex> g(mu);
     const std::vector<int> devs(devices, devices + std::max(0, ndevices));
     const bool same = cache && cache->n == n && cache->m == m && cache->l == l && cache->d == d &&

@@ -300,6 +300,24 @@ def test_anchor_planted_21_8_and_23_9():
     assert any(a["motifs"] for a in g["anchors"])
 
 
+@pytest.mark.parametrize("l,d,n,m,seed", [(7, 2, 40, 157, 1), (7, 2, 36, 150, 2), (9, 3, 36, 260, 1),
+                                          (13, 4, 40, 120, 3)])
+def test_more_than_32_sequences(l, d, n, m, seed):
+    # n > 32 (the reference takes any n): the first 32 sequences are searched,
+    # the GPU scanner keeps the motifs that occur in all n; the first three
+    # instances have far more motifs in their first 32 sequences than overall
+    inst = planted(l, d, seed, n=n, m=m)
+    want, _ = O.solve(inst.codes, l, d)
+    head, _ = O.solve(inst.codes[:32], l, d)
+    assert inst.motif in want and (l > 9 or len(head) > len(want))
+    rep = P.RunReport()
+    assert P.solve(inst.problem, P.SolverConfig(), rep) == want
+    assert P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions(devices=[0, 0])) == want
+    with pytest.raises(RuntimeError, match="motif cap"):
+        P.solve(inst.problem, P.SolverConfig(max_motifs=len(want) - 1))
+    assert P.solve(inst.problem, P.SolverConfig(max_motifs=len(want))) == want
+
+
 def test_gpu_threshold_rule():
     assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
         [2, 3, 4, 4, 7]
