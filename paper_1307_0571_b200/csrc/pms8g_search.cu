@@ -741,20 +741,28 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 // row segment; a carry chain over the non-end positions tells
                 // per segment whether it kept anything. (Rows emptied by
                 // Theorem 1 alone are found after the pass.)
+                // Rows are contiguous, so a block holds a row end iff the next
+                // block starts in another row than this one (the big rows of
+                // depth 2 span ~6 blocks: most blocks skip the row logic).
                 const uint32_t nxt_blk = __shfl_sync(0xffffffffu, e_next, 0);
-                const uint32_t nxt_lane = __shfl_down_sync(0xffffffffu, e, 1);
-                const uint32_t nxt = lane == 31 ? nxt_blk : nxt_lane;
-                const unsigned ends = __ballot_sync(0xffffffffu, valid && (nxt >> 24) != (e >> 24));
-                const unsigned balc = cb | seg_kept;
-                const unsigned mid = ~ends;
-                const unsigned nonempty = (((balc & mid) + mid) & ends) | (balc & ends);
-                if (ends & ~nonempty) {
-                    n_done = min(base + 32, n_iter);
-                    dead = true;
-                    break;
+                const uint32_t first = __shfl_sync(0xffffffffu, e, 0);
+                if ((nxt_blk >> 24) == (first >> 24)) {
+                    seg_kept |= cb != 0u ? 1u : 0u;
+                } else {
+                    const uint32_t nxt_lane = __shfl_down_sync(0xffffffffu, e, 1);
+                    const uint32_t nxt = lane == 31 ? nxt_blk : nxt_lane;
+                    const unsigned ends = __ballot_sync(0xffffffffu, valid && (nxt >> 24) != (e >> 24));
+                    const unsigned balc = cb | seg_kept;
+                    const unsigned mid = ~ends;
+                    const unsigned nonempty = (((balc & mid) + mid) & ends) | (balc & ends);
+                    if (ends & ~nonempty) {
+                        n_done = min(base + 32, n_iter);
+                        dead = true;
+                        break;
+                    }
+                    if (ends) seg_kept = (ends >> 31) ? 0u : ((cb >> (32 - __clz(ends))) != 0u ? 1u : 0u);
+                    else seg_kept |= cb != 0u ? 1u : 0u;
                 }
-                if (ends) seg_kept = (ends >> 31) ? 0u : ((cb >> (32 - __clz(ends))) != 0u ? 1u : 0u);
-                else seg_kept |= cb != 0u ? 1u : 0u;
             }
             if (cb) {
                 if (keep) {
