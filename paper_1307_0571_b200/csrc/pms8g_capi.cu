@@ -176,7 +176,7 @@ namespace {
 // context is reused only under the same values.
 std::string env_signature() {
     std::string sig;
-    for (const char* k : {"PMS8G_GLOBAL_TABLE", "PMS8G_NODE_CAP", "PMS8G_QCAP", "PMS8G_NO_TASK_ORDER"}) {
+    for (const char* k : {"PMS8G_GLOBAL_TABLE", "PMS8G_NODE_CAP", "PMS8G_QCAP", "PMS8G_NO_TASK_ORDER", "PMS8G_DON_CAP"}) {
         const char* v = std::getenv(k);
         sig += v ? v : "-";
         sig += '|';

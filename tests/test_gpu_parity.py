@@ -318,6 +318,19 @@ def test_more_than_32_sequences(l, d, n, m, seed):
     assert P.solve(inst.problem, P.SolverConfig(max_motifs=len(want))) == want
 
 
+def test_donated_tasks_replayed_without_level_handoff(monkeypatch):
+    # PMS8G_DON_CAP=0: donated tasks carry no level, receivers rebuild it by
+    # replaying the prefix pushes (the fallback for levels larger than a ring
+    # slot); few S1 l-mers per call, so most of the work is donated
+    monkeypatch.setenv("PMS8G_DON_CAP", "0")
+    _anchor_parity("anchors_21_8_planted.json", 21, 8)
+    inst = planted(36, 11, 3, n=8, m=60)
+    want, _ = O.solve(inst.codes, 36, 11)
+    for t in (4, 7):
+        assert P.solve(inst.problem, P.SolverConfig(threshold_override=t)) == want, t
+    _branch_parity("branches_50_21_planted.json")
+
+
 def test_gpu_threshold_rule():
     assert [P.gpu_threshold(20, 600, l, d) for l, d in [(13, 4), (17, 6), (21, 8), (23, 9), (50, 21)]] == \
         [2, 3, 4, 4, 7]
