@@ -15,5 +15,6 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:sear
   python scripts/profile_run.py 21 8 0 1 10 > gpurun_out/ncu_21_8.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:search_kernel -c 1 -o gpurun_out/r02m_search_17_6 -f \
   python scripts/profile_run.py 17 6 0 1 1 > gpurun_out/ncu_17_6.log 2>&1
-for cfg in "21 8 0 1 10" "17 6 0 1 1" "50 21 0 1 10" "23 9 0 1 20" "50 21 0 1 1"; do timeout 300 python scripts/profile_run.py $cfg > gpurun_out/prof_$(echo $cfg | cut -d' ' -f1-2 | tr ' ' _).txt 2>&1; done
+for cfg in "21 8 0 1 10" "17 6 0 1 1" "23 9 0 1 20" "50 21 0 1 1"; do timeout 300 python scripts/profile_run.py $cfg > gpurun_out/prof_$(echo $cfg | cut -d' ' -f1-2 | tr ' ' _).txt 2>&1; done
+PMS8G_LIB=$PWD/paper_1307_0571_b200/lib_diag/libpms8g.so timeout 300 python scripts/profile_run.py 50 21 0 1 10 2>&1 | grep -v histogram > gpurun_out/levels.txt  # -DPMS8G_LEVELSTATS build (make EXTRA=-DPMS8G_LEVELSTATS LIB=.../lib_diag)
 echo done
