@@ -1173,11 +1173,7 @@ __device__ __forceinline__ int verify_row(const WarpCtx<W, MT>& C, Lmer<W>* cand
     // entries per all-witnessed check. The t = 4 builds are bound by
     // instruction fetch (hot code > the 32 KB L1.5 I-cache): half the unroll
     // there ((21,8) -2%, (23,9) -3%; neutral for t <= 3)
-#if defined(PMS8G_VERIFY_U1)
-    constexpr int U = MT == 4 ? (NCH == 1 ? 2 : 1) : (NCH == 1 ? 8 : (NCH == 2 ? 4 : 2));
-#else
     constexpr int U = MT == 4 ? (NCH == 1 ? 4 : 2) : (NCH == 1 ? 8 : (NCH == 2 ? 4 : 2));
-#endif
     bool done = false;
     for (int eb = 0; eb < cnt && !done; eb += 32) {
         // lanes past the row's end hold a copy of its first entry, so whole
@@ -1279,11 +1275,30 @@ __device__ __noinline__ void verify_all(WarpCtx<W, MT>& C, const LevelMeta& L, c
         int scanned = 0, out = 0;
         if (n <= 12) {
             out = verify_row_small<W, MT>(C, C.cand(), entries, st, cnt, n, d, lane, scanned);
+        } else if (MT == 4) {
+            // t = 4 builds (instruction-fetch bound): one specialisation, 64
+            // candidates per pass over the row, instead of three - the row is
+            // re-read for candidates 65..160, but 3.4 KB of hot code go
+            // ((21,8) -4.5%, (23,9) -4.4%)
+            for (int g0 = 0; g0 < n; g0 += 64) {
+                const int ng = min(64, n - g0);
+                int sg = 0;
+                const int og = verify_row<W, MT, 2>(C, C.cand() + g0, entries, st, cnt, ng, d, lane, sg);
+                vcmp += static_cast<unsigned long long>(ng) * sg;
+                if (g0 > 0) {
+                    Lmer<W> mv[2];
+                    for (int q = 0; q < 2; ++q)
+                        if (q * 32 + lane < og) mv[q] = C.cand()[g0 + q * 32 + lane];
+                    __syncwarp();
+                    for (int q = 0; q < 2; ++q)
+                        if (q * 32 + lane < og) C.cand()[out + q * 32 + lane] = mv[q];
+                    __syncwarp();
+                }
+                out += og;
+            }
         } else switch ((n + 31) >> 5) {
             case 1: out = verify_row<W, MT, 1>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-#ifndef PMS8G_VERIFY_NO2
             case 2: out = verify_row<W, MT, 2>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
-#endif
             default: out = verify_row<W, MT, 5>(C, C.cand(), entries, st, cnt, n, d, lane, scanned); break;
         }
         vcmp += static_cast<unsigned long long>(n) * scanned;
