@@ -13,6 +13,7 @@ it writes are committed and travel to the GPU box.
     python tests/golden/make_golden.py heavy21      # (21,8) anchor sample
     python tests/golden/make_golden.py heavy21full  # (21,8) every S1 l-mer (~1.5 h on 8 threads)
     python tests/golden/make_golden.py heavy23      # (23,9) anchor sample
+    python tests/golden/make_golden.py heavy23more  # (23,9) 24 more S1 l-mers (t=4 override)
     python tests/golden/make_golden.py heavy50      # (50,21) depth-1 branch sample
     python tests/golden/make_golden.py heavyplanted # (21,8)/(23,9) planted S1 offsets
 """
@@ -249,6 +250,10 @@ def main():
                       threads=int(os.environ.get("GOLDEN_THREADS", THREADS)))
     elif what == "heavy23":
         anchor_sample(23, 9, 1, list(range(0, 578, 72)), "anchors_23_9.json")
+    elif what == "heavy23more":
+        # 24 more S1 l-mers of (23,9) spread over the instance, at the reference's
+        # threshold override t=4 (t-invariant motif set; faster than its t=3)
+        anchor_sample(23, 9, 1, list(range(13, 578, 24)), "anchors_23_9_more.json", t=4)
     elif what == "heavyplanted":
         # the S1 offset holding the planted occurrence in sequence 0, so the
         # heavy-config anchor parity includes a non-empty motif set
