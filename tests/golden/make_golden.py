@@ -14,6 +14,7 @@ it writes are committed and travel to the GPU box.
     python tests/golden/make_golden.py heavy21full  # (21,8) every S1 l-mer (~1.5 h on 8 threads)
     python tests/golden/make_golden.py heavy23      # (23,9) anchor sample
     python tests/golden/make_golden.py heavy23more  # (23,9) 24 more S1 l-mers (t=4 override)
+    python tests/golden/make_golden.py heavy23quarter  # (23,9) every 4th S1 l-mer (t=4 override)
     python tests/golden/make_golden.py heavy50      # (50,21) depth-1 branch sample
     python tests/golden/make_golden.py heavyplanted # (21,8)/(23,9) planted S1 offsets
 """
@@ -254,6 +255,9 @@ def main():
         # 24 more S1 l-mers of (23,9) spread over the instance, at the reference's
         # threshold override t=4 (t-invariant motif set; faster than its t=3)
         anchor_sample(23, 9, 1, list(range(13, 578, 24)), "anchors_23_9_more.json", t=4)
+    elif what == "heavy23quarter":
+        # every 4th S1 l-mer of (23,9) (144 of 578), t=4 override: ~40 min on 8 threads
+        anchor_sample(23, 9, 1, list(range(2, 578, 4)), "anchors_23_9_quarter.json", t=4)
     elif what == "heavyplanted":
         # the S1 offset holding the planted occurrence in sequence 0, so the
         # heavy-config anchor parity includes a non-empty motif set

@@ -67,6 +67,8 @@ def test_anchor_sample_21_8():
 
 def test_anchor_sample_23_9():
     _anchor_parity("anchors_23_9.json", 23, 9)
+    # 24 more S1 l-mers (reference at threshold override 4: the set is t-invariant)
+    _anchor_parity("anchors_23_9_more.json", 23, 9)
 
 
 def test_full_instance_21_8_against_every_reference_anchor():
