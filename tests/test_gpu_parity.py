@@ -295,6 +295,27 @@ def test_s1_sample_50_21():
     assert all(ok for ok, _ in P.verify_motifs(inst.problem, got))
 
 
+@pytest.mark.parametrize("l,d,seed", [(50, 21, 1), (50, 21, 2), (50, 21, 3), (23, 9, 1)])
+def test_whole_heavy_instances(l, d, seed):
+    # BASELINE's full sizes, whole instances (every S1 l-mer; (50,21) is the
+    # bench step). The reference cannot finish these, so the checks are the
+    # size-independent ones: the planted motif is in the output, the output is
+    # sorted and duplicate-free, every motif passes the CPU oracle's naive scan
+    # and the GPU scanner, and three interleaved shards union to the same set
+    inst = planted(l, d, seed)
+    got = P.run_parallel(inst.problem, P.SolverConfig(), P.ParallelOptions())
+    assert inst.motif in got
+    assert got == sorted(set(got))
+    assert all(O.is_motif(inst.codes, l, d, mo) for mo in got)
+    assert all(ok for ok, _ in P.verify_motifs(inst.problem, got))
+    if l == 50:
+        union = set()
+        for r in range(3):
+            union |= set(P.run_parallel(inst.problem, P.SolverConfig(),
+                                        P.ParallelOptions(shard_rank=r, shard_count=3)))
+        assert sorted(union) == got
+
+
 def test_anchor_planted_21_8_and_23_9():
     _anchor_parity("anchors_21_8_planted.json", 21, 8)
     _anchor_parity("anchors_23_9_planted.json", 23, 9)
