@@ -626,7 +626,9 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                    ubcnt = static_cast<uint32_t>(bcnt);
     auto load_entry = [&](int f) -> uint32_t {
         const uint32_t uf = static_cast<uint32_t>(f);  // 32-bit unsigned index: one IMAD.WIDE.U32
-        return uf < un_iter ? src[uf + (uf < ubstart ? 0u : ubcnt)] : 0xFFFFFFFFu;
+        // past the end: row 0xFF (a row change after the last entry) with id 0,
+        // so that the l-mer prefetch of a padding slot needs no select
+        return uf < un_iter ? src[uf + (uf < ubstart ? 0u : ubcnt)] : 0xFF000000u;
     };
     // software pipeline: entries two blocks ahead, their l-mers (table reads)
     // one block ahead (t >= 4 builds; the t <= 3 builds keep the one-block
@@ -639,7 +641,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
     uint32_t e_next2 = kPipeV ? load_entry(lane + 32) : 0u;
     const Lmer<W> U = tr.get(S.stack_id[k] & ID_MASK);
     Lmer<W> V_next;
-    if constexpr (kPipeV) V_next = tr.get(lane < n_iter ? e_next & ID_MASK : 0u);
+    if constexpr (kPipeV) V_next = tr.get(e_next & ID_MASK);
     StackSet<W, MT> ss;
     ss.load(C, k, U);
     const bool cons = cons_rows_at<MT>(P, k);
@@ -706,7 +708,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
             V = V_next;
             e_next = e_next2;
             e_next2 = load_entry(f + 64);
-            if (base + 32 < n_iter) V_next = tr.get(f + 32 < n_iter ? e_next & ID_MASK : 0u);
+            if (base + 32 < n_iter) V_next = tr.get(e_next & ID_MASK);
         } else {
             e_next = load_entry(f + 32);
             if (valid) V = tr.get(e & ID_MASK);
@@ -744,11 +746,13 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                 // Rows are contiguous, so a block holds a row end iff the next
                 // block starts in another row than this one (the big rows of
                 // depth 2 span ~6 blocks: most blocks skip the row logic).
-                const uint32_t nxt_blk = __shfl_sync(0xffffffffu, e_next, 0);
-                const uint32_t first = __shfl_sync(0xffffffffu, e, 0);
-                if ((nxt_blk >> 24) == (first >> 24)) {
+                // (lane 0 holds both the block's first entry and the next
+                // block's first entry: one vote instead of two broadcasts)
+                const unsigned rowdiff = __ballot_sync(0xffffffffu, ((e_next ^ e) >> 24) != 0u);
+                if (!(rowdiff & 1u)) {
                     seg_kept |= cb != 0u ? 1u : 0u;
                 } else {
+                    const uint32_t nxt_blk = __shfl_sync(0xffffffffu, e_next, 0);
                     const uint32_t nxt_lane = __shfl_down_sync(0xffffffffu, e, 1);
                     const uint32_t nxt = lane == 31 ? nxt_blk : nxt_lane;
                     const unsigned ends = __ballot_sync(0xffffffffu, valid && (nxt >> 24) != (e >> 24));
@@ -770,8 +774,10 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
                     Q.qe[qi] = e;
                 }
                 qn += __popc(cb);
-                __syncwarp();
-                if (qn >= 32) resolve(32);
+                if (qn >= 32) {
+                    __syncwarp();  // the queue stores above, before resolve reads them
+                    resolve(32);
+                }
             }
             continue;
         }
@@ -836,6 +842,7 @@ __device__ __noinline__ bool filter_push(WarpCtx<W, MT>& C, int k) {
         }
     }
     if constexpr (kQueue) {
+        __syncwarp();
         if (!dead && qn > 0) resolve(qn);
     }
     __syncwarp();
